@@ -1,0 +1,257 @@
+"""Pins of the fp64 oracle (oracle/trail_ref.py) against what the paper and mathematics
+fix: printed constants, worked examples, closed forms, invariants and textbook
+routines.  CPU only."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.special
+import torch
+
+from oracle import trail_ref as R
+from synth import workload as W
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+# ----------------------------------------------------------------------------- shape
+def test_mlp_parameter_count_matches_paper():
+    """P:362 'around 2.1 million parameters': d=4096 -> 512 -> k=10."""
+    w = W.make_weights(4096, 512, 10)
+    n = w["W1"].size + w["b1"].size + w["W2"].size + w["b2"].size
+    assert n == 4096 * 512 + 512 + 512 * 10 + 10 == 2_102_794
+    assert abs(n / 1e6 - 2.1) < 0.01
+
+
+# ----------------------------------------------------------------------------- bins
+def test_bins_and_midpoints_paper_values():
+    g = _golden("paper_bins.json")
+    e = W.paper_bin_edges(10)
+    np.testing.assert_allclose(e, g["edges"], rtol=0, atol=1e-12)
+    m = R.bin_midpoints(e)
+    # P:226 closed form m_i = 128 (2i+1) / 5 (0-based)
+    np.testing.assert_allclose(m, [128 * (2 * i + 1) / 5 for i in range(10)], atol=1e-12)
+    np.testing.assert_allclose(m, g["midpoints"], atol=1e-12)
+    assert m[0] == pytest.approx(25.6) and m[9] == pytest.approx(486.4)
+
+
+def test_transition_matrix_entries():
+    """1 - 1/51.2 = 0.98046875 and 1/51.2 = 0.01953125; binsize 2 -> 0.5/0.5;
+    k = 1 -> [1 - 1/w].  Only diagonal + the (i, i+1) entry are non-zero."""
+    T = R.transition_matrix(W.paper_bin_edges(10))
+    assert np.allclose(np.diag(T), 0.98046875, atol=1e-15)
+    assert np.allclose(np.diag(T, 1), 0.01953125, atol=1e-15)
+    mask = np.eye(10, dtype=bool) | np.eye(10, k=1, dtype=bool)
+    assert np.all(T[~mask] == 0.0)
+    T2 = R.transition_matrix(np.array([0.0, 2.0, 4.0, 6.0]))
+    assert np.allclose(np.diag(T2), 0.5) and np.allclose(np.diag(T2, 1), 0.5)
+    T1 = R.transition_matrix(np.array([0.0, 4.0]))
+    assert T1.shape == (1, 1) and T1[0, 0] == 0.75
+    # column sums: 1 except the lowest bin, which leaks 1/w_0 (D-4)
+    cs = T.sum(axis=0)
+    assert cs[0] == pytest.approx(1 - 1 / 51.2) and np.allclose(cs[1:], 1.0)
+
+
+def test_threshold_tables_paper_bins():
+    """floor(c * m_j) (D-10); c=inf never freezes (D-14)."""
+    g = _golden("paper_bins.json")
+    m = R.bin_midpoints(W.paper_bin_edges(10))
+    assert list(R.preempt_threshold(0.8, m)) == g["thr_c0.8"]
+    assert list(R.preempt_threshold(0.5, m)) == g["thr_c0.5"]
+    assert list(R.preempt_threshold(0.0, m)) == [0] * 10
+    assert np.all(R.preempt_threshold(math.inf, m) == R.UINT32_MAX)
+    # r = 8, C = 0.5 -> a0 = 4: age 3 preemptible, age 4 not
+    thr = int(R.preempt_threshold(0.5, np.array([8.0]))[0])
+    assert 3 < thr and not (4 < thr)
+    # r = 7.5, C = 0.8 -> preemptible for ages 0..5
+    thr = int(R.preempt_threshold(0.8, np.array([7.5]))[0])
+    assert [a for a in range(10) if a < thr] == [0, 1, 2, 3, 4, 5]
+
+
+def test_initial_prediction_argmax_midpoint():
+    """one-hot at (0-based) bin 2 -> 128.0; ties go to the lower bin."""
+    m = R.bin_midpoints(W.paper_bin_edges(10))
+    q = np.zeros((2, 10))
+    q[0, 2] = 1.0
+    q[1, :2] = 0.5
+    np.testing.assert_allclose(R.initial_prediction(q, m), [128.0, 25.6])
+
+
+# ----------------------------------------------------------------------------- Bayes
+def test_spec_three_bin_example():
+    """k=3, binsize 2, q_prev=[0,0,1], p=[0.2,0.5,0.3] -> [0, 0.625, 0.375];
+    with edges [0,2,4,6] (m = [1,3,5]) L = 3.75."""
+    g = _golden("spec_three_bin.json")
+    e = np.array(g["edges"])
+    T = R.transition_matrix(e)
+    q = R.bayes_update(np.array([g["q_prev"]]), np.array([g["p"]]), T)
+    np.testing.assert_allclose(q[0], g["posterior"], atol=1e-12)
+    assert R.expected_length(q, R.bin_midpoints(e))[0] == pytest.approx(g["L"], abs=1e-12)
+
+
+def test_expected_length_examples():
+    """uniform over the paper bins -> 256.0; [0.5, 0.5, 0, ...] -> 51.2."""
+    m = R.bin_midpoints(W.paper_bin_edges(10))
+    assert R.expected_length(np.full(10, 0.1), m) == pytest.approx(256.0, abs=1e-12)
+    q = np.zeros(10)
+    q[:2] = 0.5
+    assert R.expected_length(q, m) == pytest.approx(51.2, abs=1e-12)
+    assert R.prior_mean_length(W.paper_bin_edges(10), None) == pytest.approx(256.0, abs=1e-12)
+
+
+def test_uniform_prior_reduces_to_softmax():
+    """P:219 'Initialize q^(0) = p^(0)' = the general init with a uniform prior; and with
+    T = I a uniform previous posterior returns p."""
+    rs = np.random.default_rng(1)
+    z = rs.normal(size=(64, 10)) * 3
+    p = R.softmax(z)
+    np.testing.assert_allclose(p, scipy.special.softmax(z, axis=-1), rtol=1e-13, atol=1e-16)
+    q0 = R.init_posterior(p, np.full((64, 10), 0.1))
+    np.testing.assert_allclose(q0, p, rtol=1e-13)
+    q = R.bayes_update(np.full((64, 10), 0.1), p, np.eye(10))
+    np.testing.assert_allclose(q, p, rtol=1e-13)
+
+
+def test_L_minus_one_identity_pins_orientation_and_posterior_feeding():
+    """Closed form (derived in DESIGN.md §4): equal widths w, m_0 = w/2, uninformative p:
+    L' = (L - 1 + q_0/2) / (1 - q_0/w); so L' = L - 1 exactly when q_0 = 0.  The other T
+    orientation would give L + 1; a prior-fed recursion would not track q_0 of the
+    posterior.  Checked over 40 chained steps fed by the previous posterior."""
+    e = W.paper_bin_edges(10)
+    m, T, w = R.bin_midpoints(e), R.transition_matrix(e), 51.2
+    rs = np.random.default_rng(7)
+    q = rs.dirichlet(np.ones(10), size=16)
+    q[:8, 0] = 0.0
+    q /= q.sum(axis=1, keepdims=True)
+    uni = np.full_like(q, 0.1)
+    for _ in range(40):
+        L, q0 = R.expected_length(q, m), q[:, 0].copy()
+        qn = R.bayes_update(q, uni, T)
+        np.testing.assert_allclose(R.expected_length(qn, m), (L - 1 + q0 / 2) / (1 - q0 / w),
+                                   rtol=1e-12)
+        q = qn
+    # wrong orientation (transpose) moves L up by one for mass away from the top bin
+    q = np.zeros((1, 10))
+    q[0, 4] = 1.0
+    up = R.bayes_update(q, np.full((1, 10), 0.1), T.T)
+    assert R.expected_length(up, m)[0] == pytest.approx(R.expected_length(q, m)[0] + 1, abs=1e-9)
+
+
+def test_posterior_on_simplex_and_L_in_range():
+    e = W.paper_bin_edges(10)
+    m, T = R.bin_midpoints(e), R.transition_matrix(e)
+    rs = np.random.default_rng(3)
+    q = R.softmax(rs.normal(size=(128, 10)) * 4)
+    for _ in range(300):
+        q = R.bayes_update(q, R.softmax(rs.normal(size=(128, 10)) * 4), T)
+        assert np.all(q >= 0) and np.allclose(q.sum(axis=1), 1.0, atol=1e-12)
+        L = R.expected_length(q, m)
+        assert np.all(L >= m[0] - 1e-9) and np.all(L <= m[-1] + 1e-9)
+
+
+def test_linear_and_log_domain_agree():
+    """D-22: the linear fp64 recursion equals its log-domain form to <= 1e-12 over 200
+    confident, contradictory (adversarial iid) observations."""
+    e = W.paper_bin_edges(10)
+    T = R.transition_matrix(e)
+    rs = np.random.default_rng(11)
+    z = rs.normal(size=(64, 10)) * 4
+    q = R.softmax(z)
+    lq = np.log(q)
+    worst = 0.0
+    for _ in range(200):
+        z = rs.normal(size=(64, 10)) * 4
+        p = R.softmax(z)
+        logp = z - scipy.special.logsumexp(z, axis=1, keepdims=True)
+        q = R.bayes_update(q, p, T)
+        lq = R.bayes_update_log(lq, logp, T)
+        worst = max(worst, float(np.abs(q - np.exp(lq)).max()))
+    assert worst <= 1e-12
+
+
+def test_refinement_beats_raw_on_noisy_observations():
+    """Property stand-in for Fig. 3: with noisy per-iteration
+    observations around the true remaining length, the refined estimate's mean absolute
+    error is below the raw per-iteration estimate's; with noiseless observations the two
+    coincide in the lowest bin's quantisation error only."""
+    e = W.paper_bin_edges(10)
+    m, T = R.bin_midpoints(e), R.transition_matrix(e)
+    rs = np.random.default_rng(5)
+    raw_err, ref_err = [], []
+    for _ in range(300):
+        N = int(rs.integers(20, 500))
+        q = None
+        for t in range(N):
+            rem = N - t
+            score = -2.0 * np.abs(m - rem) / 51.2 + rs.normal(0, 1.5, 10)
+            p = R.softmax(score[None, :])
+            q = p if q is None else R.bayes_update(q, p, T)
+            raw_err.append(abs(R.expected_length(p, m)[0] - rem))
+            ref_err.append(abs(R.expected_length(q, m)[0] - rem))
+    assert np.mean(ref_err) < 0.8 * np.mean(raw_err)
+
+
+# ----------------------------------------------------------------------------- MLP, pool
+def test_classifier_against_torch_fp64():
+    """h = ReLU(W1 x + b1), z = W2 h + b2 against torch.nn in fp64."""
+    rs = np.random.default_rng(2)
+    d, H, k, n = 64, 32, 10, 9
+    W1, b1 = rs.normal(size=(H, d)), rs.normal(size=H)
+    W2, b2 = rs.normal(size=(k, H)), rs.normal(size=k)
+    X = rs.normal(size=(n, d))
+    net = torch.nn.Sequential(torch.nn.Linear(d, H), torch.nn.ReLU(), torch.nn.Linear(H, k)).double()
+    with torch.no_grad():
+        net[0].weight.copy_(torch.from_numpy(W1)); net[0].bias.copy_(torch.from_numpy(b1))
+        net[2].weight.copy_(torch.from_numpy(W2)); net[2].bias.copy_(torch.from_numpy(b2))
+        ref = net(torch.from_numpy(X)).numpy()
+    np.testing.assert_allclose(R.classifier_logits(X, W1, b1, W2, b2), ref, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(R.softmax(ref), torch.softmax(torch.from_numpy(ref), -1).numpy(),
+                               rtol=1e-12)
+
+
+def test_bf16_round_matches_torch_and_synth():
+    rs = np.random.default_rng(4)
+    x = np.concatenate([rs.normal(size=20000).astype(np.float32),
+                        (rs.normal(size=2000) * 1e-30).astype(np.float32),
+                        np.array([1.0, 1.00390625, 1.005859375, 3.0e38, -2.5], np.float32)])
+    ours = R.bf16_round(x.astype(np.float64))
+    tor = torch.from_numpy(x).to(torch.bfloat16).to(torch.float64).numpy()
+    np.testing.assert_array_equal(ours, tor)
+    np.testing.assert_array_equal(ours, W.bf16_bits_to_f32(W.f32_to_bf16_bits(x)).astype(np.float64))
+
+
+def test_pool_mean_and_decode_row():
+    rs = np.random.default_rng(6)
+    rows = W.bf16_bits_to_f32(W.f32_to_bf16_bits(rs.normal(size=(44, 128)))).astype(np.float64)
+    np.testing.assert_array_equal(R.pool_embedding(rows[:1], "bf16"), rows[0])   # decode row exact
+    u = R.pool_embedding(rows, "bf16")
+    assert np.all(np.abs(u - rows.mean(axis=0)) <= np.abs(rows.mean(axis=0)) * 2 ** -8 + 1e-30)
+    np.testing.assert_array_equal(R.pool_embedding(rows, "f32"), rows.mean(axis=0))
+
+
+# ----------------------------------------------------------------------------- the step
+def test_oracle_step_semantics():
+    """Prefill initialises q, r, thr, a=0; each decode applies one update and a += 1;
+    the key of an unseen request is E_pi[L]; forced iff running & seen & a >= thr."""
+    d, k = 64, 10
+    w = W.make_weights(d, 32, k, "f32")
+    o = R.TrailOracle(w["W1"], w["b1"], w["W2"], w["b2"], w["edges"], 0.8, 8, x_dtype="f32")
+    rs = np.random.default_rng(0)
+    emb = rs.normal(size=(5, d))
+    q, L = o.predict_step(emb, np.array([0, 4, 5]), np.array([1, 3]), np.array([1, 1]))
+    assert np.all(o.state.age[[1, 3]] == 0) and o.state.seen[[1, 3]].all()
+    thr0 = o.state.thr[[1, 3]].copy()
+    q2, L2 = o.predict_step(emb[:2], np.array([0, 1, 2]), np.array([1, 3]), np.array([0, 0]))
+    assert np.all(o.state.age[[1, 3]] == 1) and np.all(o.state.thr[[1, 3]] == thr0)
+    p = o.probs(emb[:2])
+    np.testing.assert_allclose(q2, R.bayes_update(q, p, o.T), rtol=1e-14)
+    key, forced = o.keys_and_forced(np.array([1, 3, 5]), np.array([1, 1, 0]))
+    assert key[2] == pytest.approx(256.0) and not forced[2]
+    assert list(forced[:2]) == [bool(1 >= t) for t in thr0]
