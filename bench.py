@@ -1,0 +1,505 @@
+#!/usr/bin/env python
+"""bench.py — TRAIL predict+schedule step on B200 (BASELINE.json metric: predict+schedule
+requests/s and us/iteration; % HBM/TC roofline).
+
+One STEP = one pass of the whole hot path over one iteration's
+batch: trail_predict_step for the n running requests of this GPU (gather/mean-pool,
+layer 1, head with Bayes refinement and expected length) + trail_schedule_step for all
+live requests (record pack, NCCL all-gather of records when N > 1, global selection).
+
+Default workload = BASELINE.json configs[1] ("c2"): 512 requests per GPU (+128 waiting),
+Llama-3-8B-shaped d = 4096 bf16 layer-11 embeddings, MLP 4096->512->10 bins, Bayesian
+refinement, limited-preemption SRPT c = 0.8 under a KV-block budget.  At N > 1 every
+rank holds 512 requests (configs[2] at N = 8: 4096 requests over 8 B200): weak scaling.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c4] [--impl ours|reference]
+
+Inputs are synthetic (synth/, seeded) and resident in HBM before the timed region; L2 is
+flushed (256 MiB memset) between timed steps, outside the per-step CUDA-event brackets.
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import workload as W  # noqa: E402
+
+CONFIGS = {
+    # name: (n per GPU, waiting per GPU, d, H, k, dtype, c, bins_total, description)
+    "c2": dict(n=512, waiting=128, d=4096, H=512, k=10, dtype="bf16", c=0.8, total=512.0,
+               desc="512 req/GPU, bf16 Llama-3-8B-shaped layer-11 embeddings d=4096, MLP "
+                    "4096->512->10, Bayes refinement + limited-preemption SRPT c=0.8 under a "
+                    "KV block budget"),
+    "c1": dict(n=64, waiting=16, d=4096, H=512, k=10, dtype="f32", c=0.8, total=512.0,
+               desc="64 running requests, d=4096, MLP 4096->512->10, fp32"),
+    "c4": dict(n=16384, waiting=4096, d=8192, H=512, k=20, dtype="bf16", c=0.8, total=1024.0,
+               desc="16384 requests/GPU at d=8192 (70B-shaped), 20 bins, tcgen05 GEMM regime"),
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), float(j["bf16_tflops"]), float(j.get("bf16_tflops_sustained", j["bf16_tflops"])), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- workload
+def make_batches(cfg, nb: int, rank: int, world: int, seed: int):
+    """nb consecutive iterations of the scripted engine (open loop): burst prefill first,
+    then decode with Alpaca-like completions/arrivals."""
+    eng = W.EngineScript(cfg["n"], cfg["waiting"], d=cfg["d"], dtype=cfg["dtype"],
+                         seed=seed + 1000 * rank, arrival_base=rank, arrival_stride=world)
+    batches = []
+    for _ in range(nb):
+        batches.append(eng.batch())
+        eng.advance()
+    return eng, batches
+
+
+def to_dev(a, torch, device):
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint32:
+        a = a.view(np.int32)
+    return torch.from_numpy(a).to(device)
+
+
+def algorithmic_bytes_l1(cfg, n):
+    eb = 2 if cfg["dtype"] == "bf16" else 4
+    return cfg["H"] * cfg["d"] * eb + n * cfg["d"] * eb
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    from paper_2410_01035_b200 import (Trail, load_library, trail_comm_init,
+                                       trail_nccl_unique_id, trail_plan_l1,
+                                       trail_profile_enable, trail_profile_read)
+    load_library()
+    hbm, tf_burst, tf_sust, peak_src = peaks()
+
+    nb = max(1, min(args.distinct, args.steps + args.warmup))
+    eng, batches = make_batches(cfg, nb, rank, world, args.seed)
+    w = W.make_weights(cfg["d"], cfg["H"], cfg["k"], cfg["dtype"],
+                       edges=W.paper_bin_edges(cfg["k"], cfg["total"]), seed=args.seed)
+    max_slots = eng.max_slots
+    t = Trail(w, cfg["c"], max_slots, max_slots, max_slots, dtype=cfg["dtype"], device=local,
+              world_size=world, id_base=rank * max_slots)
+    if world > 1:
+        uid = [trail_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        trail_comm_init(t.h, uid[0], rank, world)
+
+    # device-resident inputs for every distinct iteration
+    dev = [dict(emb=to_dev(b.emb, torch, device), off=to_dev(b.row_offsets, torch, device),
+                ids=to_dev(b.request_ids, torch, device), pref=to_dev(b.is_prefill, torch, device),
+                sids=to_dev(b.sched_ids, torch, device), arr=to_dev(b.arrival_seq, torch, device),
+                kv=to_dev(b.kv_blocks, torch, device), run=to_dev(b.is_running, torch, device),
+                budget=b.kv_budget, n=b.n, m=b.m, rows=int(b.row_offsets[-1]))
+           for b in batches]
+    stream = torch.cuda.Stream(device)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+
+    def step(i):
+        x = dev[i % nb]
+        t.predict(x["emb"], x["off"], x["ids"], x["pref"], stream=stream)
+        t.schedule(x["sids"], x["arr"], x["kv"], x["run"], x["budget"], stream=stream)
+
+    # first pass over the distinct batches eagerly: burst prefill initialises the slots
+    with torch.cuda.stream(stream):
+        for i in range(nb):
+            step(i)
+    torch.cuda.synchronize()
+
+    # CUDA graphs per distinct batch, with per-kernel event nodes (profile mode 2)
+    trail_profile_enable(t.h, 2)
+    use_graph = not args.no_graph
+    graphs = []
+    if use_graph:
+        for i in range(nb):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                step(i)
+            graphs.append(g)
+        torch.cuda.synchronize()
+
+    def run_step(i):
+        if use_graph:
+            with torch.cuda.stream(stream):
+                graphs[i % nb].replay()
+        else:
+            with torch.cuda.stream(stream):
+                step(i)
+
+    kernels = ["pool", "gemv", "umma", "head", "pack", "select", "gather"]
+    for i in range(args.warmup):
+        run_step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    kern_ms = {k: [] for k in kernels}
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            if not args.no_flush:
+                with torch.cuda.stream(stream):
+                    flush.zero_()
+            ev[i][0].record(stream)
+            run_step(args.warmup + i)
+            ev[i][1].record(stream)
+            stream.synchronize()
+            for kname in kernels:
+                ms, cnt = trail_profile_read(t.h, kname)
+                if cnt:
+                    kern_ms[kname].append(ms)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / args.steps
+    n_total = cfg["n"] * world
+    value = n_total / (ms_per_step / 1e3)
+
+    # ---- roofline of the dominant kernel
+    avg = {k: (sum(v) / len(v)) for k, v in kern_ms.items() if v}
+    dom = max(avg, key=avg.get) if avg else None
+    n_avg = float(np.mean([x["n"] for x in dev]))
+    mode, splits = trail_plan_l1(t.h, int(n_avg))
+    roof = None
+    if dom in ("umma", "gemv"):
+        byts = algorithmic_bytes_l1(cfg, n_avg)
+        flops = 2.0 * n_avg * cfg["d"] * cfg["H"]
+        t_s = avg[dom] / 1e3
+        ach_bw = byts / t_s / 1e9
+        ach_tf = flops / t_s / 1e12
+        # at n = 512 the contraction sits at the bf16 ridge (I = 254 vs 259 flop/B): report
+        # the bound whose fraction is larger
+        if dom == "umma" and ach_tf / tf_sust > ach_bw / hbm:
+            roof = {"bound": "tensor", "achieved": ach_tf, "peak": tf_sust, "unit": "TFLOP/s",
+                    "frac": ach_tf / tf_sust}
+        else:
+            roof = {"bound": "hbm", "achieved": ach_bw, "peak": hbm, "unit": "GB/s",
+                    "frac": ach_bw / hbm}
+    elif dom == "pool":
+        byts = float(np.mean([(x["rows"] + x["n"]) * cfg["d"] * (2 if cfg["dtype"] == "bf16" else 4)
+                              for x in dev]))
+        ach = byts / (avg[dom] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
+    elif dom is not None:
+        # latency-bound kernel (head / select): report against the HBM roof of its bytes
+        byts = 16.0 * float(np.mean([x["m"] for x in dev])) * world * 3
+        ach = byts / (avg[dom] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
+    if roof is not None:
+        roof.update({"kernel": dom, "peak_source": peak_src, "avg_launch_us": avg[dom] * 1e3,
+                     "traffic": None,
+                     "kernel_us": {k: round(v * 1e3, 3) for k, v in avg.items()},
+                     "share_of_step": avg[dom] / ms_per_step})
+
+    # ---- end to end through the C ABI with HOST buffers (pinned), copies in the timed region
+    e2e = run_e2e(args, cfg, t, batches, stream, flush, torch, device, world)
+
+    # ---- gpu launches of our kernels in the timed region
+    per_step = 5  # pool, layer-1 (GEMV or tcgen05), head, pack, select
+    gpu_launches = per_step * args.steps
+
+    out = None
+    if rank == 0:
+        cpu = cpu_baseline(cfg, args) if (world == 1 and not args.no_cpu) else None
+        out = {
+            "metric": "predict+schedule requests/s",
+            "value": value,
+            "unit": "requests/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "us_per_iteration": ms_per_step * 1e3,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": cfg["dtype"],
+            "data": "synthetic (seeded; random-init probe of the paper's shape)",
+            "config": {
+                "workload": f"BASELINE configs[{ {'c1': 0, 'c2': 1, 'c4': 3}[args.config] }]" +
+                            (f" / configs[2] shape at N={world}" if world > 1 else "") +
+                            ": " + cfg["desc"],
+                "n_per_gpu": cfg["n"], "waiting_per_gpu": cfg["waiting"], "d": cfg["d"],
+                "hidden": cfg["H"], "bins": cfg["k"], "c": cfg["c"],
+                "l1_kernel": {1: "gemv", 2: "tcgen05"}[mode], "l1_splits": splits,
+                "l2": "flushed between timed steps (256 MiB memset outside the step events)"
+                      if not args.no_flush else "warm",
+                "cuda_graph": use_graph,
+                "parallelism": f"request-sharded x{world}, replicated weights" +
+                               (", NCCL all-gather of 16 B records, identical global selection"
+                                if world > 1 else ""),
+            },
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "clocks": clk.summary(),
+        }
+    t.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def run_e2e(args, cfg, t, batches, stream, flush, torch, device, world):
+    """Same metric through the public API with pinned HOST inputs/outputs: per step the H2D
+    copy of that step's inputs, predict + schedule, and the D2H read of posteriors, expected
+    lengths, counts and the three lists, all inside the per-step CUDA-event bracket."""
+    nb = len(batches)
+    host = []
+    for b in batches:
+        h = {}
+        for name, arr in (("emb", b.emb), ("off", b.row_offsets), ("ids", b.request_ids),
+                          ("pref", b.is_prefill), ("sids", b.sched_ids), ("arr", b.arrival_seq),
+                          ("kv", b.kv_blocks), ("run", b.is_running)):
+            a = np.ascontiguousarray(arr)
+            if a.dtype == np.uint32:
+                a = a.view(np.int32)
+            h[name] = torch.from_numpy(a).pin_memory()
+        h["budget"], h["n"], h["m"] = b.kv_budget, b.n, b.m
+        host.append(h)
+    dbuf = {k: torch.empty(max(v.numel() for v in (hh[k] for hh in host)), dtype=host[0][k].dtype,
+                           device=device) for k in host[0] if isinstance(host[0][k], torch.Tensor)}
+    cap = t.run_ids.numel()
+    out_host = {"post": torch.empty_like(t.post, device="cpu").pin_memory(),
+                "L": torch.empty_like(t.L, device="cpu").pin_memory(),
+                "counts": torch.empty(4, dtype=torch.int32).pin_memory(),
+                "lists": torch.empty(3 * cap, dtype=torch.int32).pin_memory()}
+    lists_dev = torch.empty(3 * cap, dtype=torch.int32, device=device)
+
+    def step(i):
+        h = host[i % nb]
+        n, m = h["n"], h["m"]
+        views = {}
+        for k, v in h.items():
+            if isinstance(v, torch.Tensor):
+                dv = dbuf[k][: v.numel()]
+                dv.copy_(v, non_blocking=True)
+                views[k] = dv.view(v.shape)
+        t.predict(views["emb"].view(-1, cfg["d"]) if cfg["dtype"] == "f32" else views["emb"],
+                  views["off"], views["ids"], views["pref"], stream=stream)
+        t.schedule(views["sids"], views["arr"], views["kv"], views["run"], h["budget"],
+                   stream=stream)
+        lists_dev[:cap].copy_(t.run_ids)
+        lists_dev[cap:2 * cap].copy_(t.preempt_ids)
+        lists_dev[2 * cap:].copy_(t.admit_ids)
+        out_host["post"][:n].copy_(t.post[:n], non_blocking=True)
+        out_host["L"][:n].copy_(t.L[:n], non_blocking=True)
+        out_host["counts"].copy_(t.counts, non_blocking=True)
+        out_host["lists"].copy_(lists_dev, non_blocking=True)
+        h2d = sum(v.numel() * v.element_size() for v in h.values() if isinstance(v, torch.Tensor))
+        d2h = n * cfg["k"] * 4 + n * 4 + 16 + 3 * cap * 4
+        return h2d, d2h
+
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+    torch.cuda.synchronize()
+    steps = max(3, min(args.steps, 50))
+    tot, h2d_b, d2h_b = 0.0, 0, 0
+    for i in range(steps):
+        with torch.cuda.stream(stream):
+            if not args.no_flush:
+                flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            h2d, d2h = step(args.warmup + i)
+            b.record(stream)
+        stream.synchronize()
+        tot += a.elapsed_time(b)
+        h2d_b += h2d
+        d2h_b += d2h
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([tot], dtype=torch.float64, device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tot = float(tt.item())
+    ms = tot / steps
+    return {"value": cfg["n"] * world / (ms / 1e3), "unit": "requests/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(h2d_b / steps), "d2h_bytes_per_step": int(d2h_b / steps),
+            "steps": steps}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def _threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return 1
+
+
+def oracle_steps(cfg, args, seconds: float, max_steps: int):
+    from oracle import trail_ref as R
+    eng, batches = make_batches(cfg, max_steps, 0, 1, args.seed)
+    w = W.make_weights(cfg["d"], cfg["H"], cfg["k"], cfg["dtype"],
+                       edges=W.paper_bin_edges(cfg["k"], cfg["total"]), seed=args.seed)
+    o = R.TrailOracle(W.decode(w["W1"], cfg["dtype"]), w["b1"], w["W2"], w["b2"], w["edges"],
+                      cfg["c"], eng.max_slots, x_dtype=cfg["dtype"])
+    emb64 = [W.decode(b.emb, cfg["dtype"]) for b in batches]
+    times, reqs = [], 0
+    t_start = time.perf_counter()
+    for i, b in enumerate(batches):
+        t0 = time.perf_counter()
+        o.predict_step(emb64[i], b.row_offsets, b.request_ids, b.is_prefill)
+        o.schedule_step(b.sched_ids, b.arrival_seq, b.kv_blocks, b.is_running, b.kv_budget)
+        times.append(time.perf_counter() - t0)
+        reqs += b.n
+        if time.perf_counter() - t_start > seconds:
+            break
+    return times, reqs
+
+
+def cpu_baseline(cfg, args):
+    times, reqs = oracle_steps(cfg, args, seconds=args.cpu_seconds, max_steps=64)
+    tot = sum(times)
+    return {"value": reqs / tot, "unit": "requests/s", "cores": _threads(), "kind": "oracle",
+            "ms_per_step": 1e3 * tot / len(times),
+            "sample": f"{len(times)} full steps of the same workload (numpy fp64 oracle, "
+                      f"{cfg['n']} predicted + {cfg['n'] + cfg['waiting']} scheduled requests "
+                      f"each), {tot:.1f} s of CPU work on {os.cpu_count()} host CPUs"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if rank != 0:
+        return None
+    times, reqs = oracle_steps(cfg, args, seconds=1e9, max_steps=args.warmup + args.steps)
+    times = times[args.warmup:] if len(times) > args.warmup else times
+    n_steps = len(times)
+    tot = sum(times)
+    ms = 1e3 * tot / n_steps
+    val = cfg["n"] / (ms / 1e3)
+    return {
+        "impl": "reference",
+        "metric": "predict+schedule requests/s", "value": val, "unit": "requests/s",
+        "n_gpus": world, "steps": n_steps, "warmup": args.warmup, "ms_per_step": ms,
+        "us_per_iteration": ms * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+        "config": {"workload": cfg["desc"], "n_per_gpu": cfg["n"], "d": cfg["d"], "bins": cfg["k"],
+                   "c": cfg["c"], "note": "the fp64 CPU oracle (oracle/trail_ref.py) is the "
+                                          "reference arm: the paper ships no code"},
+        "cpu_baseline": {"value": val, "unit": "requests/s", "cores": _threads(), "kind": "oracle",
+                         "sample": f"{n_steps} full steps, rank 0 only"},
+        "e2e": {"value": val, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--distinct", type=int, default=16, help="distinct iterations cycled")
+    ap.add_argument("--seed", type=int, default=W.MASTER_SEED)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    out = run_reference(args, cfg) if args.impl == "reference" else run_ours(args, cfg)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,222 @@
+/* trail.h — C ABI of libtrail.so: TRAIL's per-iteration predict+schedule hot path on
+ * B200 (sm_100a).  arXiv 2410.01035; citations P:<line> refer to PAPER.md.
+ *
+ * Conventions (apply to every entry point)
+ *   - Every data pointer is a DEVICE pointer unless marked (host).  Device buffers are
+ *     owned by the caller; the library never frees or retains them past the call.
+ *   - Every call enqueues work on `stream` (a cudaStream_t; NULL = legacy default stream)
+ *     and returns without synchronising, unless documented as synchronising.  Outputs are
+ *     valid once the stream reaches that point.  Calls are CUDA-graph capturable (no
+ *     allocation, no host synchronisation, no host reads of device data).
+ *   - A handle is not thread-safe: one host thread (and one stream at a time) per handle.
+ *   - Return value: TRAIL_OK, or a negative trail_status.  A negative status means the
+ *     call was rejected on the host before any work was enqueued and no state changed.
+ *     Errors that can only be seen on the device (an id >= max_slots, an empty row range,
+ *     a negative KV count, a non-finite length) set sticky bits readable with
+ *     trail_device_errors(); the offending request is skipped or clamped as documented.
+ *   - No exceptions cross the ABI.
+ */
+#ifndef TRAIL_H_
+#define TRAIL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TRAIL_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define TRAIL_API __attribute__((visibility("default")))
+#else
+#define TRAIL_API
+#endif
+
+typedef struct trail_ctx *trail_handle;
+typedef struct CUstream_st *trail_stream; /* == cudaStream_t */
+
+typedef enum {
+  TRAIL_OK = 0,
+  TRAIL_WARN_OVER_BUDGET = 1,  /* forced (non-preemptible) set alone exceeds budget/cap */
+  TRAIL_ERR_INVALID = -1,      /* bad argument (shape, pointer, alignment, value)       */
+  TRAIL_ERR_CUDA = -2,         /* a CUDA runtime/driver call failed                      */
+  TRAIL_ERR_NOMEM = -3,        /* device or host allocation failed                       */
+  TRAIL_ERR_CAPACITY = -4,     /* n exceeds the capacity fixed at trail_create            */
+  TRAIL_ERR_NCCL = -5,         /* NCCL unavailable or a collective failed                */
+  TRAIL_ERR_STATE = -6,        /* call not valid in the handle's current state            */
+  TRAIL_ERR_UNSUPPORTED = -7   /* configuration outside what this build implements       */
+} trail_status;
+
+typedef enum { TRAIL_F32 = 0, TRAIL_BF16 = 1 } trail_dtype;
+
+/* Layer-1 kernel selection (row a2). */
+typedef enum {
+  TRAIL_L1_AUTO = 0,   /* GEMV for fp32 or small n, tcgen05 GEMM otherwise */
+  TRAIL_L1_GEMV = 1,   /* K2a: warp-per-output-slice split-K GEMV (CUDA cores) */
+  TRAIL_L1_UMMA = 2    /* K2b: TMA-fed tcgen05/TMEM GEMM (bf16 only) */
+} trail_l1_mode;
+
+/* Sticky device-side error bits (trail_device_errors). */
+#define TRAIL_DEV_BAD_ID   0x1u   /* request id >= max_slots: request skipped            */
+#define TRAIL_DEV_BAD_ROWS 0x2u   /* row range empty or reversed: treated as a zero row   */
+#define TRAIL_DEV_NEG_KV   0x4u   /* kv_blocks < 0: treated as 0                          */
+#define TRAIL_DEV_NONFIN   0x8u   /* non-finite expected length: key encoded as +inf      */
+
+typedef struct {
+  /* Classifier (Linear(d, 512) - ReLU - Linear(512, k); P:362 ~2.1M params). */
+  int32_t d;               /* embedding width; multiple of 64 (bf16) or 8 (fp32)          */
+  int32_t hidden;          /* probe width H; multiple of 128, <= 512 (paper: 512)         */
+  int32_t k;               /* number of bins, 1..32 (paper: 10)                           */
+  int32_t dtype;           /* trail_dtype of W1 and of the embeddings                     */
+  const void *w1;          /* (host) [hidden][d] row-major (nn.Linear [out][in]), dtype   */
+  const float *b1;         /* (host) [hidden]                                             */
+  const float *w2;         /* (host) [k][hidden] row-major                                */
+  const float *b2;         /* (host) [k]                                                  */
+  /* Bins: B_i = [b_i, b_{i+1}), last bin closed; widths >= 1 token.  */
+  const double *bin_edges; /* (host) [k+1] strictly increasing, b_0 >= 0                 */
+  const double *prior;     /* (host) [k] prior pi on the simplex, or NULL = uniform       */
+  double c;                /* limited preemption: preemptible while a < floor(c*r);
+                              c >= 0; INFINITY = unlimited (reading D-14)                  */
+  /* Capacities (fixed for the handle's lifetime). */
+  int32_t max_slots;       /* request ids are slot indices in [0, max_slots)              */
+  int32_t max_requests;    /* max n per trail_predict_step                                */
+  int32_t max_sched;       /* max records per trail_schedule_step on THIS rank            */
+  int32_t world_size;      /* ranks sharing one selection (1 = single GPU)                */
+  uint32_t id_base;        /* added to slot ids in the returned lists (e.g. rank*max_slots) */
+  int32_t device;          /* CUDA device ordinal the handle lives on                     */
+  int32_t l1_mode;         /* trail_l1_mode                                               */
+} trail_config;
+
+/* Library ABI version (TRAIL_ABI_VERSION). */
+TRAIL_API int32_t trail_abi_version(void);
+
+/* Validates cfg, copies weights and constants to library-owned device memory and
+ * precomputes in fp64 on the host: bin midpoints m_i, the transition
+ * coefficients log(1-1/w_i) and log(1/w_{i+1}) of T (reading D-1), the
+ * threshold table floor(c*m_j) (D-10) and E_pi[L] (D-24).  Allocates per-slot
+ * state (all slots unobserved) and step workspaces.  Synchronising.
+ * Errors: TRAIL_ERR_INVALID (shapes, non-increasing edges, width < 1, prior not on the
+ * simplex, c < 0 or NaN), TRAIL_ERR_NOMEM, TRAIL_ERR_CUDA. */
+TRAIL_API trail_status trail_create(const trail_config *cfg, trail_handle *out);
+
+/* Frees everything the handle owns (and its NCCL communicator).  Synchronising. */
+TRAIL_API trail_status trail_destroy(trail_handle h);
+
+/* One prediction iteration for the n requests that just ran.
+ *   emb            [rows][emb_ld] in cfg.dtype: the layer-l hidden states of the flat
+ *                  token batch, 16-byte aligned, emb_ld a multiple of 8 (bf16) /
+ *                  4 (fp32) elements, emb_ld >= d.
+ *   row_offsets    [n+1] int32 CSR: request j owns rows [row_offsets[j], row_offsets[j+1]).
+ *                  A decode observation has 1 row (its new token); a prefill
+ *                  observation has its prompt rows, which are mean-pooled (D-12).
+ *   request_ids    [n] slot ids, unique within the call.
+ *   is_prefill     [n] 1 = first observation of the request: q^(0) = normalise(pi * p)
+ *                  (P:219), r = m[argmax q^(0)], threshold = floor(c r), age a = 0.
+ *                  0 = decode: q = normalise((T q_prev) * p) (D-2), a += 1.
+ *                  A decode on a never-observed slot is treated as a prefill (D-23).
+ *   prior_override [n][k] fp32 per-request prior pi for prefill rows, or NULL.
+ *   posteriors     [n][k] fp32 out (may be NULL): q^(t) of each request.
+ *   expected_remaining [n] fp32 out (may be NULL): L_t = sum_i q(i) m_i.
+ * Updates the per-slot state (log q in fp32, reading D-22; a; threshold; L_t). */
+TRAIL_API trail_status trail_predict_step(trail_handle h, const void *emb, int64_t emb_ld,
+                                const int32_t *row_offsets, const uint32_t *request_ids,
+                                const uint8_t *is_prefill, const float *prior_override,
+                                int32_t n, float *posteriors, float *expected_remaining,
+                                trail_stream stream);
+
+/* Next-batch selection: limited-preemption SPRPT under a KV-block budget (P:171, P:394,
+ * P:570).  Inputs are THIS rank's live requests (running + waiting):
+ *   request_ids  [n] slot ids;  arrival_seq [n] arrival order (FCFS tie-break),
+ *                globally unique across ranks;  kv_blocks [n] >= 0 blocks the request needs
+ *                resident to run the next iteration;  is_running [n] 1 = in the batch that
+ *                just ran.
+ *   kv_budget    blocks available to the run set;  max_run  cap on the run-set size (0 =
+ *                no cap).
+ * Key = L_t of the slot (E_pi[L] if never observed, D-24).  A request is forced
+ * (non-preemptible, rank -inf) iff running, observed and a >= floor(c r).
+ * Order: forced first, then ascending key, then arrival_seq.  Run set = all forced +
+ * the longest prefix of the rest that keeps the cumulative KV within the budget and the
+ * count within max_run (strict prefix, D-15).  If the forced set alone violates either
+ * limit, run = forced and status TRAIL_WARN_OVER_BUDGET (D-16).
+ * With world_size > 1 (after trail_comm_init) the 16-byte records of all ranks are
+ * all-gathered over NCCL and every rank computes the identical global selection.
+ * Outputs (ids are id_base + slot of the owning rank, in priority order):
+ *   run_ids, preempt_ids, admit_ids  capacity max_sched * world_size each;
+ *   counts[4] = {n_run, n_preempt (running, not in run), n_admit (waiting, in run), status}.
+ * The returned status reports host-side validation only; the selection's own status
+ * (TRAIL_OK / TRAIL_WARN_OVER_BUDGET) is counts[3] on the device. */
+TRAIL_API trail_status trail_schedule_step(trail_handle h, const uint32_t *request_ids,
+                                 const uint32_t *arrival_seq, const int32_t *kv_blocks,
+                                 const uint8_t *is_running, int32_t n, int64_t kv_budget,
+                                 int32_t max_run, uint32_t *run_ids, uint32_t *preempt_ids,
+                                 uint32_t *admit_ids, int32_t *counts, trail_stream stream);
+
+/* The two halves of trail_schedule_step, for callers that run their own collective.
+ * pack writes n 16-byte records {u32 keybits, u32 arrival_seq, u32 kv_blocks,
+ * u32 (id_base+slot) | running<<31} where keybits = (!forced)<<31 | fp32 bits of the key.
+ * select consumes n_records such records (from any number of ranks, any order; records
+ * with keybits == 0xFFFFFFFF are padding and ignored). */
+TRAIL_API trail_status trail_schedule_pack(trail_handle h, const uint32_t *request_ids,
+                                 const uint32_t *arrival_seq, const int32_t *kv_blocks,
+                                 const uint8_t *is_running, int32_t n, void *records,
+                                 trail_stream stream);
+TRAIL_API trail_status trail_schedule_select(trail_handle h, const void *records, int32_t n_records,
+                                   int64_t kv_budget, int32_t max_run, uint32_t *run_ids,
+                                   uint32_t *preempt_ids, uint32_t *admit_ids,
+                                   int32_t *counts, trail_stream stream);
+
+/* Marks n slots as never observed (finished requests). */
+TRAIL_API trail_status trail_release(trail_handle h, const uint32_t *request_ids, int32_t n,
+                           trail_stream stream);
+
+/* Reads per-slot state for n ids (any output may be NULL): L_t, age a, threshold
+ * floor(c r), seen flag, and the posterior q (fp32 [n][k], = exp of the log state). */
+TRAIL_API trail_status trail_read_state(trail_handle h, const uint32_t *request_ids, int32_t n,
+                              float *L, uint32_t *age, uint32_t *threshold, uint8_t *seen,
+                              float *posterior, trail_stream stream);
+
+/* Multi-GPU: NCCL unique id (128 bytes, host) generated on rank 0 and broadcast by the
+ * caller; then every rank calls trail_comm_init.  NCCL is loaded at run time
+ * (libnccl.so.2); TRAIL_ERR_NCCL if it is unavailable.  Synchronising. */
+TRAIL_API trail_status trail_nccl_unique_id(void *id_out /* (host) 128 bytes */);
+TRAIL_API trail_status trail_comm_init(trail_handle h, const void *id /* (host) 128 bytes */,
+                             int32_t rank, int32_t world_size);
+
+/* Sticky device error bits (TRAIL_DEV_*); synchronising; clear != 0 resets them. */
+TRAIL_API trail_status trail_device_errors(trail_handle h, uint32_t *bits_out, int32_t clear);
+
+/* Per-kernel timing with CUDA events on the launch stream.  enable: 0 = off;
+ * 1 = accumulate: trail_profile_read returns, for kernel id `kid` (TRAIL_K_*), the summed
+ *     device time in ms and the number of launches since the last reset;
+ * 2 = last launch (CUDA-graph friendly: one event pair per kernel id, re-recorded on
+ *     every launch, including by event-record nodes of a graph captured in this mode):
+ *     trail_profile_read returns the duration of the most recent launch of `kid`.
+ * trail_profile_read is synchronising. */
+#define TRAIL_K_POOL 0
+#define TRAIL_K_GEMV 1
+#define TRAIL_K_UMMA 2
+#define TRAIL_K_HEAD 3
+#define TRAIL_K_PACK 4
+#define TRAIL_K_SELECT 5
+#define TRAIL_K_GATHER 6
+#define TRAIL_K_COUNT 7
+TRAIL_API trail_status trail_profile_enable(trail_handle h, int32_t enable);
+TRAIL_API trail_status trail_profile_read(trail_handle h, int32_t kid, double *total_ms,
+                                int64_t *launches, int32_t reset);
+
+/* Overrides cfg.l1_mode for subsequent calls (TRAIL_L1_UMMA requires bf16). */
+TRAIL_API trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode);
+
+/* Which layer-1 kernel trail_predict_step uses for n requests, and its split-K factor. */
+TRAIL_API trail_status trail_plan_l1(trail_handle h, int32_t n, int32_t *l1_mode_out,
+                           int32_t *splits_out);
+
+/* Human-readable message for a status. */
+TRAIL_API const char *trail_status_string(trail_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRAIL_H_ */

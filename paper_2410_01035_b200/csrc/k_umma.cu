@@ -1,0 +1,274 @@
+// K2b — classifier layer 1 on the 5th-generation tensor cores (row a2, bf16, large n).
+//
+// P:201 "The first layer maps the input embedding to a 512-dimensional space": with n
+// requests this is the dense contraction D[n][H] = X[n][d] . W1[H][d]^T (a "TN" GEMM, both
+// operands K-major).  One CTA computes a 128 x BN tile (BN = 128 or 256 hidden units) over
+// the K range of its split s (grid = m_tiles x H/BN x S, sized to one wave of the 148 SMs):
+//   warp 0 / lane 0 : TMA producer — cp.async.bulk.tensor 2-D loads of a 128x64 X tile and a
+//                     BNx64 W1 tile per stage into 128-byte-swizzled shared memory, arriving
+//                     on the stage's mbarrier with complete_tx;
+//   warp 1 / lane 0 : MMA issuer — tcgen05.mma.cta_group::1.kind::f16 (bf16 x bf16 -> fp32,
+//                     M=128, N=BN, K=16) x 4 per stage into a TMEM accumulator of BN columns;
+//                     tcgen05.commit frees the stage, and a final commit signals the epilogue;
+//   warps 0-3       : epilogue — tcgen05.ld 32x32b.x32 (warp w owns TMEM lanes 32w..32w+31 =
+//                     tile rows), fp32 partial sums written to partial[s][row][n0 + col].
+// Bias, ReLU and the fixed-order reduction over splits are fused into the head kernel K3,
+// which keeps h in fp32 (D-22 note: rounding h to bf16 breaks the 2e-3 posterior bound).
+#include <stdio.h>
+
+#include "trail_internal.cuh"
+
+namespace trail {
+
+namespace {
+constexpr int BM = 128;
+constexpr int BK = 64;   // one 128-byte swizzle atom of bf16 per row
+
+template <int BN>
+struct UCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_BYTES = 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + BAR_BYTES + 1024;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+// Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): K-major operand, rows of
+// 128 bytes, 128-byte swizzle, 8-row core-matrix groups 1024 bytes apart.
+__device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);   // start address >> 4
+  d |= (uint64_t)1 << 16;                    // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;          // stride byte offset: next 8-row group
+  d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                    // layout: SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+}  // namespace
+
+template <int BN>
+__global__ void __launch_bounds__(128, 1)
+trail_umma_l1_kernel(const __grid_constant__ CUtensorMap tmap_x,
+                     const __grid_constant__ CUtensorMap tmap_w, int n, int H, int kblocks,
+                     int splits, float *__restrict__ partial) {
+  using C = UCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t *sA = smem;
+  uint8_t *sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sB + C::STAGES * C::B_BYTES);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * C::STAGES + 1);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + C::STAGES),
+                 done = smem_u32(bars + 2 * C::STAGES);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN, s = blockIdx.z;
+  const int kb0 = (int)((int64_t)s * kblocks / splits);
+  const int kb1 = (int)((int64_t)(s + 1) * kblocks / splits);
+  const int nkb = kb1 - kb0;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(full0 + 8 * i, 1);
+      mbar_init(empty0 + 8 * i, 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_w)) : "memory");
+  }
+  if (warp == 0) {  // whole warp: allocate BN fp32 columns of tensor memory
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"((uint32_t)BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    for (int i = 0; i < nkb; ++i) {
+      const int st = i % C::STAGES;
+      const uint32_t ph = (uint32_t)(i / C::STAGES) & 1u;
+      mbar_wait(empty0 + 8 * st, ph ^ 1u);
+      mbar_expect_tx(full0 + 8 * st, C::STAGE_BYTES);
+      const int kc = (kb0 + i) * BK;
+      tma_load_2d(smem_u32(sA + st * C::A_BYTES), &tmap_x, full0 + 8 * st, kc, m0);
+      tma_load_2d(smem_u32(sB + st * C::B_BYTES), &tmap_w, full0 + 8 * st, kc, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer (single thread)
+    constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+    for (int i = 0; i < nkb; ++i) {
+      const int st = i % C::STAGES;
+      const uint32_t ph = (uint32_t)(i / C::STAGES) & 1u;
+      mbar_wait(full0 + 8 * st, ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t da = sw128_kmajor_desc(smem_u32(sA + st * C::A_BYTES));
+      const uint64_t db = sw128_kmajor_desc(smem_u32(sB + st * C::B_BYTES));
+#pragma unroll
+      for (int kk = 0; kk < BK / 16; ++kk)   // +32 bytes along K inside the swizzle atom
+        umma_bf16(tmem, da + 2 * kk, db + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+      umma_commit(empty0 + 8 * st);
+    }
+    umma_commit(done);
+  }
+  // ---------------- epilogue: TMEM -> registers -> fp32 partials
+  mbar_wait(done, 0);
+  __syncwarp();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int row = m0 + warp * 32 + lane;
+  float *dst = partial + ((int64_t)s * n + row) * H + n0;
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 32) {
+    uint32_t r[32];
+    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, r);
+    if (row < n) {
+      float4 *d4 = reinterpret_cast<float4 *>(dst + c);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        d4[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                            __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"((uint32_t)BN)
+                 : "memory");
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                    const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                    const cuuint32_t *, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled)p;
+  }
+  return fn;
+}
+
+static bool encode_2d_bf16(CUtensorMap *m, const void *base, uint64_t inner, uint64_t outer,
+                           uint32_t box_inner, uint32_t box_outer) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+cudaError_t umma_prepare(Ctx &c) {
+  if (c.dtype != TRAIL_BF16) return cudaSuccess;
+  if (!encode_2d_bf16(&c.tmap_x, c.xs, (uint64_t)c.d, (uint64_t)c.cfg.max_requests, BK, BM) ||
+      !encode_2d_bf16(&c.tmap_w128, c.w1, (uint64_t)c.d, (uint64_t)c.H, BK, 128) ||
+      (c.H % 256 == 0 &&
+       !encode_2d_bf16(&c.tmap_w256, c.w1, (uint64_t)c.d, (uint64_t)c.H, BK, 256)))
+    return cudaErrorInvalidValue;
+  c.have_tmaps = true;
+  cudaError_t e = cudaFuncSetAttribute(trail_umma_l1_kernel<128>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, UCfg<128>::SMEM);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(trail_umma_l1_kernel<256>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, UCfg<256>::SMEM);
+}
+
+int umma_max_bn(const Ctx &c) { return c.H % 256 == 0 ? 256 : 128; }
+
+cudaError_t launch_umma_l1(const Ctx &c, int n, int bn, int splits, cudaStream_t s) {
+  if (!c.have_tmaps) return cudaErrorInvalidValue;
+  const int kblocks = c.d / BK;
+  dim3 grid((n + BM - 1) / BM, c.H / bn, splits);
+  if (bn == 256)
+    trail_umma_l1_kernel<256><<<grid, 128, UCfg<256>::SMEM, s>>>(c.tmap_x, c.tmap_w256, n, c.H,
+                                                                kblocks, splits, c.partial);
+  else
+    trail_umma_l1_kernel<128><<<grid, 128, UCfg<128>::SMEM, s>>>(c.tmap_x, c.tmap_w128, n, c.H,
+                                                                kblocks, splits, c.partial);
+  return cudaGetLastError();
+}
+
+}  // namespace trail

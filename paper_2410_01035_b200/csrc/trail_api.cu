@@ -1,0 +1,555 @@
+// trail_api.cu — the C ABI of libtrail.so (include/trail.h): argument validation, the
+// create-time constants (computed in fp64 on the host), workspace ownership, layer-1
+// regime planning, NCCL all-gather of records (NCCL loaded at run time), profiling.
+#include <dlfcn.h>
+#include <math.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+
+#include "trail_internal.cuh"
+
+using namespace trail;
+
+struct trail_ctx {
+  Ctx c;
+};
+
+namespace {
+
+constexpr int kGemvMaxN = 16;   // AUTO: GEMV up to this many requests (bf16)
+
+#define TRAIL_CUDA(expr)                                                     \
+  do {                                                                       \
+    cudaError_t _e = (expr);                                                 \
+    if (_e != cudaSuccess) {                                                 \
+      fprintf(stderr, "[trail] %s failed: %s\n", #expr, cudaGetErrorString(_e)); \
+      return TRAIL_ERR_CUDA;                                                 \
+    }                                                                        \
+  } while (0)
+
+struct ProfScope {
+  Ctx &c;
+  int slot = -1;
+  cudaStream_t s;
+  int kid_ = -1;
+  ProfScope(Ctx &c_, int kid, cudaStream_t s_) : c(c_), s(s_) {
+    if (!c.prof) return;
+    if (c.prof_mode == 2) {
+      kid_ = kid;
+      c.last_used[kid] = true;
+      cudaEventRecord(c.last_ev[kid][0], s);
+    } else if (c.prof_n < c.prof_cap) {
+      slot = c.prof_n++;
+      c.prof_kid[slot] = kid;
+      cudaEventRecord(c.prof_ev[2 * slot], s);
+    }
+  }
+  ~ProfScope() {
+    if (kid_ >= 0) cudaEventRecord(c.last_ev[kid_][1], s);
+    else if (slot >= 0) cudaEventRecord(c.prof_ev[2 * slot + 1], s);
+  }
+};
+
+void plan_l1(const Ctx &c, int n, int *mode, int *bn, int *splits) {
+  int m = c.cfg.l1_mode;
+  if (c.dtype == TRAIL_F32) m = TRAIL_L1_GEMV;
+  else if (m == TRAIL_L1_AUTO) m = (n <= kGemvMaxN) ? TRAIL_L1_GEMV : TRAIL_L1_UMMA;
+  if (m == TRAIL_L1_GEMV) {
+    const int ctas_x = c.H / 16;
+    const int vec = c.dtype == TRAIL_BF16 ? 8 : 4;
+    int s = std::max(1, (2 * c.num_sms) / ctas_x);
+    s = std::min(s, std::max(1, c.d / (vec * 32)));
+    *mode = TRAIL_L1_GEMV;
+    *bn = 0;
+    *splits = s;
+  } else {
+    const int b = (n > 1024 && umma_max_bn(c) == 256) ? 256 : 128;
+    const int tiles = ((n + 127) / 128) * (c.H / b);
+    const int kblocks = c.d / 64;
+    *mode = TRAIL_L1_UMMA;
+    *bn = b;
+    *splits = std::max(1, std::min(kblocks, c.num_sms / std::max(1, tiles)));
+  }
+}
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+  void *lib = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char *(*errStr)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+NcclApi &nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char *nm : names) {
+      api.lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (api.lib) break;
+    }
+    if (api.lib) {
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(api.lib, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(api.lib, "ncclCommInitRank");
+      api.allGather = (decltype(api.allGather))dlsym(api.lib, "ncclAllGather");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(api.lib, "ncclCommDestroy");
+      api.errStr = (decltype(api.errStr))dlsym(api.lib, "ncclGetErrorString");
+      api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy;
+    }
+  }
+  return api;
+}
+
+trail_status set_device(const Ctx &c) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess) return TRAIL_ERR_CUDA;
+  if (cur != c.device && cudaSetDevice(c.device) != cudaSuccess) return TRAIL_ERR_CUDA;
+  return TRAIL_OK;
+}
+
+void free_ctx(Ctx &c) {
+  void *ptrs[] = {c.w1, c.b1, c.w2, c.b2, c.consts, c.lq, c.meta, c.dev_err, c.xs,
+                  c.partial, c.rec_local, c.rec_all, c.sel_scratch};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  if (c.prof_ev) {
+    for (int i = 0; i < 2 * c.prof_cap; ++i) cudaEventDestroy(c.prof_ev[i]);
+    delete[] c.prof_ev;
+    delete[] c.prof_kid;
+  }
+  for (int i = 0; i < TRAIL_K_COUNT; ++i)
+    for (int j = 0; j < 2; ++j)
+      if (c.last_ev[i][j]) cudaEventDestroy(c.last_ev[i][j]);
+  if (c.nccl_comm && nccl().ok) nccl().commDestroy((ncclComm_t)c.nccl_comm);
+}
+
+size_t partial_elems_needed(const Ctx &c) {
+  size_t best = 0;
+  for (int n = 1; n <= c.cfg.max_requests; ++n) {
+    for (int forced = 0; forced < 2; ++forced) {
+      Ctx tmp_c;
+      tmp_c.cfg = c.cfg;
+      tmp_c.cfg.l1_mode = forced ? TRAIL_L1_GEMV : TRAIL_L1_UMMA;
+      if (c.dtype == TRAIL_F32 && !forced) continue;
+      tmp_c.d = c.d; tmp_c.H = c.H; tmp_c.dtype = c.dtype; tmp_c.num_sms = c.num_sms;
+      int mode, bn, s;
+      plan_l1(tmp_c, n, &mode, &bn, &s);
+      best = std::max(best, (size_t)s * (size_t)n * (size_t)c.H);
+    }
+  }
+  return best;
+}
+
+}  // namespace
+
+// =============================================================================== ABI
+extern "C" {
+
+int32_t trail_abi_version(void) { return TRAIL_ABI_VERSION; }
+
+const char *trail_status_string(trail_status s) {
+  switch (s) {
+    case TRAIL_OK: return "ok";
+    case TRAIL_WARN_OVER_BUDGET: return "forced set exceeds the KV budget or run cap";
+    case TRAIL_ERR_INVALID: return "invalid argument";
+    case TRAIL_ERR_CUDA: return "CUDA error";
+    case TRAIL_ERR_NOMEM: return "out of memory";
+    case TRAIL_ERR_CAPACITY: return "capacity exceeded";
+    case TRAIL_ERR_NCCL: return "NCCL unavailable or failed";
+    case TRAIL_ERR_STATE: return "invalid handle state";
+    case TRAIL_ERR_UNSUPPORTED: return "unsupported configuration";
+  }
+  return "unknown status";
+}
+
+trail_status trail_create(const trail_config *cfg, trail_handle *out) {
+  if (!cfg || !out) return TRAIL_ERR_INVALID;
+  *out = nullptr;
+  const trail_config &g = *cfg;
+  if (g.dtype != TRAIL_F32 && g.dtype != TRAIL_BF16) return TRAIL_ERR_INVALID;
+  if (g.k < 1 || g.k > kMaxBins) return TRAIL_ERR_INVALID;
+  if (g.hidden < 128 || g.hidden > kMaxHidden || g.hidden % 128) return TRAIL_ERR_INVALID;
+  if (g.d <= 0 || (g.dtype == TRAIL_BF16 ? g.d % 64 : g.d % 8)) return TRAIL_ERR_INVALID;
+  if (!g.w1 || !g.b1 || !g.w2 || !g.b2 || !g.bin_edges) return TRAIL_ERR_INVALID;
+  if (!(g.c >= 0.0)) return TRAIL_ERR_INVALID;   // rejects NaN and negatives
+  if (g.max_slots <= 0 || g.max_requests <= 0 || g.max_sched < 0) return TRAIL_ERR_INVALID;
+  if (g.world_size < 1) return TRAIL_ERR_INVALID;
+  if (g.l1_mode < 0 || g.l1_mode > 2) return TRAIL_ERR_INVALID;
+  if (g.l1_mode == TRAIL_L1_UMMA && g.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
+  if ((int64_t)g.max_sched * g.world_size > (1 << 26)) return TRAIL_ERR_INVALID;
+  const int k = g.k;
+  const double *e = g.bin_edges;
+  if (!(e[0] >= 0.0)) return TRAIL_ERR_INVALID;
+  for (int i = 0; i < k; ++i)
+    if (!(e[i + 1] - e[i] >= 1.0) || !isfinite(e[i + 1])) return TRAIL_ERR_INVALID;
+  double prior[kMaxBins];
+  if (g.prior) {
+    double s = 0;
+    for (int i = 0; i < k; ++i) {
+      if (!(g.prior[i] >= 0.0)) return TRAIL_ERR_INVALID;
+      s += g.prior[i];
+    }
+    if (fabs(s - 1.0) > 1e-6) return TRAIL_ERR_INVALID;
+    for (int i = 0; i < k; ++i) prior[i] = g.prior[i] / s;
+  } else {
+    for (int i = 0; i < k; ++i) prior[i] = 1.0 / k;
+  }
+
+  trail_ctx *h = new (std::nothrow) trail_ctx();
+  if (!h) return TRAIL_ERR_NOMEM;
+  Ctx &c = h->c;
+  c.cfg = g;
+  c.device = g.device;
+  c.d = g.d; c.H = g.hidden; c.k = k; c.dtype = g.dtype;
+  c.esize = g.dtype == TRAIL_BF16 ? 2 : 4;
+  c.world = g.world_size;
+  auto fail = [&](trail_status st) { free_ctx(c); delete h; return st; };
+  if (cudaSetDevice(c.device) != cudaSuccess) return fail(TRAIL_ERR_CUDA);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, c.device) != cudaSuccess) return fail(TRAIL_ERR_CUDA);
+  if (prop.major < 10) {
+    fprintf(stderr, "[trail] device %d is sm_%d%d; this library is built for sm_100a\n", c.device,
+            prop.major, prop.minor);
+    return fail(TRAIL_ERR_UNSUPPORTED);
+  }
+  c.num_sms = prop.multiProcessorCount;
+
+  // ---- constants in fp64
+  HeadConsts &hc = c.host_consts;
+  memset(&hc, 0, sizeof(hc));
+  hc.k = k;
+  hc.H = c.H;
+  double prior_L = 0.0;
+  for (int i = 0; i < kMaxBins; ++i) {
+    if (i < k) {
+      const double m = (e[i] + e[i + 1]) * 0.5;
+      const double w = e[i + 1] - e[i];
+      hc.m[i] = (float)m;
+      hc.log_stay[i] = (float)log(1.0 - 1.0 / w);
+      hc.log_move[i] = (i + 1 < k) ? (float)log(1.0 / (e[i + 2] - e[i + 1])) : -INFINITY;
+      hc.log_prior[i] = prior[i] > 0 ? (float)log(prior[i]) : -INFINITY;
+      if (isinf(g.c)) {
+        hc.thr_tab[i] = 0xFFFFFFFFu;
+      } else {
+        const double t = floor(g.c * m);
+        hc.thr_tab[i] = t >= 4294967295.0 ? 0xFFFFFFFEu : (uint32_t)t;
+      }
+      prior_L += prior[i] * m;
+    } else {
+      hc.m[i] = 0.f; hc.log_stay[i] = -INFINITY; hc.log_move[i] = -INFINITY;
+      hc.log_prior[i] = -INFINITY; hc.thr_tab[i] = 0xFFFFFFFFu;
+    }
+  }
+  hc.prior_L = (float)prior_L;
+
+  // ---- device memory
+  const size_t w1_bytes = (size_t)c.H * c.d * c.esize;
+#define ALLOC(ptr, bytes) \
+  if (cudaMalloc((void **)&(ptr), (bytes)) != cudaSuccess) return fail(TRAIL_ERR_NOMEM)
+  ALLOC(c.w1, w1_bytes);
+  ALLOC(c.b1, c.H * sizeof(float));
+  ALLOC(c.w2, (size_t)k * c.H * sizeof(float));
+  ALLOC(c.b2, k * sizeof(float));
+  ALLOC(c.consts, sizeof(HeadConsts));
+  ALLOC(c.lq, (size_t)g.max_slots * k * sizeof(float));
+  ALLOC(c.meta, (size_t)g.max_slots * sizeof(SlotMeta));
+  ALLOC(c.dev_err, sizeof(uint32_t));
+  ALLOC(c.xs, (size_t)g.max_requests * c.d * c.esize);
+  c.partial_elems = partial_elems_needed(c);
+  ALLOC(c.partial, c.partial_elems * sizeof(float));
+  const int max_sched = std::max(1, g.max_sched);
+  ALLOC(c.rec_local, (size_t)max_sched * sizeof(Record));
+  if (c.world > 1) ALLOC(c.rec_all, (size_t)max_sched * c.world * sizeof(Record));
+  c.sel_scratch_bytes = select_scratch_bytes(max_sched * c.world);
+  if (c.sel_scratch_bytes) ALLOC(c.sel_scratch, c.sel_scratch_bytes);
+#undef ALLOC
+  if (cudaMemcpy(c.w1, g.w1, w1_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(c.b1, g.b1, c.H * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(c.w2, g.w2, (size_t)k * c.H * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(c.b2, g.b2, k * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(c.consts, &hc, sizeof(hc), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemset(c.lq, 0, (size_t)g.max_slots * k * sizeof(float)) != cudaSuccess ||
+      cudaMemset(c.meta, 0, (size_t)g.max_slots * sizeof(SlotMeta)) != cudaSuccess ||
+      cudaMemset(c.dev_err, 0, sizeof(uint32_t)) != cudaSuccess ||
+      cudaMemset(c.xs, 0, (size_t)g.max_requests * c.d * c.esize) != cudaSuccess)
+    return fail(TRAIL_ERR_CUDA);
+  if (umma_prepare(c) != cudaSuccess || head_prepare(c) != cudaSuccess ||
+      select_prepare(c) != cudaSuccess)
+    return fail(TRAIL_ERR_CUDA);
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(TRAIL_ERR_CUDA);
+  *out = h;
+  return TRAIL_OK;
+}
+
+trail_status trail_destroy(trail_handle h) {
+  if (!h) return TRAIL_ERR_INVALID;
+  set_device(h->c);
+  cudaDeviceSynchronize();
+  free_ctx(h->c);
+  delete h;
+  return TRAIL_OK;
+}
+
+trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode) {
+  if (!h || l1_mode < 0 || l1_mode > 2) return TRAIL_ERR_INVALID;
+  if (l1_mode == TRAIL_L1_UMMA && h->c.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
+  h->c.cfg.l1_mode = l1_mode;
+  return TRAIL_OK;
+}
+
+trail_status trail_plan_l1(trail_handle h, int32_t n, int32_t *l1_mode_out, int32_t *splits_out) {
+  if (!h || n < 0) return TRAIL_ERR_INVALID;
+  int mode, bn, s;
+  plan_l1(h->c, std::max(1, n), &mode, &bn, &s);
+  if (l1_mode_out) *l1_mode_out = mode;
+  if (splits_out) *splits_out = s;
+  return TRAIL_OK;
+}
+
+trail_status trail_predict_step(trail_handle h, const void *emb, int64_t emb_ld,
+                                const int32_t *row_offsets, const uint32_t *request_ids,
+                                const uint8_t *is_prefill, const float *prior_override,
+                                int32_t n, float *posteriors, float *expected_remaining,
+                                trail_stream stream) {
+  if (!h) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (n < 0) return TRAIL_ERR_INVALID;
+  if (n == 0) return TRAIL_OK;
+  if (n > c.cfg.max_requests) return TRAIL_ERR_CAPACITY;
+  if (!emb || !row_offsets || !request_ids || !is_prefill) return TRAIL_ERR_INVALID;
+  if (emb_ld < c.d || (emb_ld * (int64_t)c.esize) % 16 != 0 || ((uintptr_t)emb) % 16 != 0)
+    return TRAIL_ERR_INVALID;
+  if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  int mode, bn, splits;
+  plan_l1(c, n, &mode, &bn, &splits);
+  if ((size_t)splits * n * c.H > c.partial_elems) return TRAIL_ERR_CAPACITY;
+  {
+    ProfScope p(c, TRAIL_K_POOL, s);
+    TRAIL_CUDA(launch_pool(c, emb, emb_ld, row_offsets, n, s));
+  }
+  if (mode == TRAIL_L1_GEMV) {
+    ProfScope p(c, TRAIL_K_GEMV, s);
+    TRAIL_CUDA(launch_gemv_l1(c, n, splits, s));
+  } else {
+    ProfScope p(c, TRAIL_K_UMMA, s);
+    TRAIL_CUDA(launch_umma_l1(c, n, bn, splits, s));
+  }
+  {
+    ProfScope p(c, TRAIL_K_HEAD, s);
+    TRAIL_CUDA(launch_head(c, n, splits, request_ids, is_prefill, prior_override, posteriors,
+                           expected_remaining, s));
+  }
+  return TRAIL_OK;
+}
+
+trail_status trail_schedule_pack(trail_handle h, const uint32_t *request_ids,
+                                 const uint32_t *arrival_seq, const int32_t *kv_blocks,
+                                 const uint8_t *is_running, int32_t n, void *records,
+                                 trail_stream stream) {
+  if (!h || n < 0) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (n == 0) return TRAIL_OK;
+  if (!request_ids || !arrival_seq || !kv_blocks || !is_running || !records)
+    return TRAIL_ERR_INVALID;
+  if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  ProfScope p(c, TRAIL_K_PACK, s);
+  TRAIL_CUDA(launch_pack(c, request_ids, arrival_seq, kv_blocks, is_running, n, (Record *)records,
+                         n, s));
+  return TRAIL_OK;
+}
+
+trail_status trail_schedule_select(trail_handle h, const void *records, int32_t n_records,
+                                   int64_t kv_budget, int32_t max_run, uint32_t *run_ids,
+                                   uint32_t *preempt_ids, uint32_t *admit_ids,
+                                   int32_t *counts, trail_stream stream) {
+  if (!h || n_records < 0 || max_run < 0) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (!counts || (n_records > 0 && (!records || !run_ids || !preempt_ids || !admit_ids)))
+    return TRAIL_ERR_INVALID;
+  if ((int64_t)n_records > (int64_t)std::max(1, c.cfg.max_sched) * c.world)
+    return TRAIL_ERR_CAPACITY;
+  if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  ProfScope p(c, TRAIL_K_SELECT, s);
+  TRAIL_CUDA(launch_select(c, (const Record *)records, n_records, kv_budget, max_run, run_ids,
+                           preempt_ids, admit_ids, counts, s));
+  return TRAIL_OK;
+}
+
+trail_status trail_schedule_step(trail_handle h, const uint32_t *request_ids,
+                                 const uint32_t *arrival_seq, const int32_t *kv_blocks,
+                                 const uint8_t *is_running, int32_t n, int64_t kv_budget,
+                                 int32_t max_run, uint32_t *run_ids, uint32_t *preempt_ids,
+                                 uint32_t *admit_ids, int32_t *counts, trail_stream stream) {
+  if (!h || n < 0 || max_run < 0) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (n > std::max(0, c.cfg.max_sched)) return TRAIL_ERR_CAPACITY;
+  if (!counts || !run_ids || !preempt_ids || !admit_ids) return TRAIL_ERR_INVALID;
+  if (n > 0 && (!request_ids || !arrival_seq || !kv_blocks || !is_running))
+    return TRAIL_ERR_INVALID;
+  if (c.world > 1 && !c.nccl_comm) return TRAIL_ERR_STATE;
+  if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int npad = c.world > 1 ? std::max(1, c.cfg.max_sched) : n;
+  {
+    ProfScope p(c, TRAIL_K_PACK, s);
+    TRAIL_CUDA(launch_pack(c, request_ids, arrival_seq, kv_blocks, is_running, n, c.rec_local,
+                           npad, s));
+  }
+  const Record *sel_in = c.rec_local;
+  int total = n;
+  if (c.world > 1) {
+    NcclApi &api = nccl();
+    ProfScope p(c, TRAIL_K_GATHER, s);
+    ncclResult_t r = api.allGather(c.rec_local, c.rec_all, (size_t)npad * sizeof(Record),
+                                   ncclUint8, (ncclComm_t)c.nccl_comm, s);
+    if (r != ncclSuccess) {
+      fprintf(stderr, "[trail] ncclAllGather: %s\n", api.errStr ? api.errStr(r) : "?");
+      return TRAIL_ERR_NCCL;
+    }
+    sel_in = c.rec_all;
+    total = npad * c.world;
+  }
+  ProfScope p(c, TRAIL_K_SELECT, s);
+  TRAIL_CUDA(launch_select(c, sel_in, total, kv_budget, max_run, run_ids, preempt_ids, admit_ids,
+                           counts, s));
+  return TRAIL_OK;
+}
+
+trail_status trail_release(trail_handle h, const uint32_t *request_ids, int32_t n,
+                           trail_stream stream) {
+  if (!h || n < 0) return TRAIL_ERR_INVALID;
+  if (n == 0) return TRAIL_OK;
+  if (!request_ids) return TRAIL_ERR_INVALID;
+  if (set_device(h->c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  TRAIL_CUDA(launch_release(h->c, request_ids, n, (cudaStream_t)stream));
+  return TRAIL_OK;
+}
+
+trail_status trail_read_state(trail_handle h, const uint32_t *request_ids, int32_t n, float *L,
+                              uint32_t *age, uint32_t *threshold, uint8_t *seen,
+                              float *posterior, trail_stream stream) {
+  if (!h || n < 0) return TRAIL_ERR_INVALID;
+  if (n == 0) return TRAIL_OK;
+  if (!request_ids) return TRAIL_ERR_INVALID;
+  if (set_device(h->c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  TRAIL_CUDA(launch_read_state(h->c, request_ids, n, L, age, threshold, seen, posterior,
+                               (cudaStream_t)stream));
+  return TRAIL_OK;
+}
+
+trail_status trail_nccl_unique_id(void *id_out) {
+  if (!id_out) return TRAIL_ERR_INVALID;
+  NcclApi &api = nccl();
+  if (!api.ok) return TRAIL_ERR_NCCL;
+  ncclUniqueId id;
+  if (api.getUniqueId(&id) != ncclSuccess) return TRAIL_ERR_NCCL;
+  memcpy(id_out, &id, sizeof(id));
+  return TRAIL_OK;
+}
+
+trail_status trail_comm_init(trail_handle h, const void *id, int32_t rank, int32_t world_size) {
+  if (!h || !id || rank < 0 || world_size < 1 || rank >= world_size) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (world_size != c.world) return TRAIL_ERR_INVALID;
+  if (c.nccl_comm) return TRAIL_ERR_STATE;
+  NcclApi &api = nccl();
+  if (!api.ok) return TRAIL_ERR_NCCL;
+  if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t comm;
+  ncclResult_t r = api.commInitRank(&comm, world_size, uid, rank);
+  if (r != ncclSuccess) {
+    fprintf(stderr, "[trail] ncclCommInitRank: %s\n", api.errStr ? api.errStr(r) : "?");
+    return TRAIL_ERR_NCCL;
+  }
+  c.nccl_comm = comm;
+  c.rank = rank;
+  return TRAIL_OK;
+}
+
+trail_status trail_device_errors(trail_handle h, uint32_t *bits_out, int32_t clear) {
+  if (!h || !bits_out) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  TRAIL_CUDA(cudaDeviceSynchronize());
+  TRAIL_CUDA(cudaMemcpy(bits_out, c.dev_err, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  if (clear) TRAIL_CUDA(cudaMemset(c.dev_err, 0, sizeof(uint32_t)));
+  return TRAIL_OK;
+}
+
+trail_status trail_profile_enable(trail_handle h, int32_t enable) {
+  if (!h) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (enable == 2) {
+    if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+    for (int i = 0; i < TRAIL_K_COUNT; ++i)
+      for (int j = 0; j < 2; ++j)
+        if (!c.last_ev[i][j]) TRAIL_CUDA(cudaEventCreate(&c.last_ev[i][j]));
+    c.prof_mode = 2;
+    c.prof = true;
+    return TRAIL_OK;
+  }
+  c.prof_mode = enable ? 1 : 0;
+  if (enable && !c.prof_ev) {
+    if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+    c.prof_cap = 8192;
+    c.prof_ev = new (std::nothrow) cudaEvent_t[2 * c.prof_cap];
+    c.prof_kid = new (std::nothrow) int[c.prof_cap];
+    if (!c.prof_ev || !c.prof_kid) return TRAIL_ERR_NOMEM;
+    for (int i = 0; i < 2 * c.prof_cap; ++i) TRAIL_CUDA(cudaEventCreate(&c.prof_ev[i]));
+  }
+  c.prof = enable != 0;
+  return TRAIL_OK;
+}
+
+trail_status trail_profile_read(trail_handle h, int32_t kid, double *total_ms, int64_t *launches,
+                                int32_t reset) {
+  if (!h || kid < 0 || kid >= TRAIL_K_COUNT) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (c.prof_mode == 2) {   // duration of the most recent launch of `kid`
+    double ms = 0.0;
+    int64_t cnt = 0;
+    if (c.last_used[kid]) {
+      float f = 0.f;
+      TRAIL_CUDA(cudaEventSynchronize(c.last_ev[kid][1]));
+      TRAIL_CUDA(cudaEventElapsedTime(&f, c.last_ev[kid][0], c.last_ev[kid][1]));
+      ms = f;
+      cnt = 1;
+    }
+    if (total_ms) *total_ms = ms;
+    if (launches) *launches = cnt;
+    return TRAIL_OK;
+  }
+  if (c.prof_n > 0) {
+    TRAIL_CUDA(cudaEventSynchronize(c.prof_ev[2 * (c.prof_n - 1) + 1]));
+    for (int i = 0; i < c.prof_n; ++i) {
+      float ms = 0.f;
+      TRAIL_CUDA(cudaEventElapsedTime(&ms, c.prof_ev[2 * i], c.prof_ev[2 * i + 1]));
+      c.prof_ms[c.prof_kid[i]] += ms;
+      c.prof_cnt[c.prof_kid[i]] += 1;
+    }
+    c.prof_n = 0;
+  }
+  if (total_ms) *total_ms = c.prof_ms[kid];
+  if (launches) *launches = c.prof_cnt[kid];
+  if (reset) {
+    for (int i = 0; i < TRAIL_K_COUNT; ++i) { c.prof_ms[i] = 0; c.prof_cnt[i] = 0; }
+  }
+  return TRAIL_OK;
+}
+
+}  // extern "C"

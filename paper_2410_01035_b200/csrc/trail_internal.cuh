@@ -1,0 +1,126 @@
+// trail_internal.cuh — shared definitions of libtrail.so (CUDA path only; the oracle
+// under oracle/ shares nothing with this file).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/trail.h"
+
+namespace trail {
+
+constexpr int kMaxBins = 32;      // one warp lane per bin in the head kernel
+constexpr int kMaxHidden = 512;   // TMEM columns (fp32) of one 128-row accumulator
+constexpr int kRecordBytes = 16;
+constexpr uint32_t kPadKey = 0xFFFFFFFFu;
+
+// Per-slot state (16 B) + log-posterior row [k] kept separately.
+struct SlotMeta {
+  float L;          // expected remaining length L_t
+  uint32_t age;     // decode iterations since the first observation (D-11)
+  uint32_t thr;     // floor(c * r) (D-10); 0xFFFFFFFF = never frozen
+  uint32_t flags;   // bit0 = observed
+};
+
+struct Record {     // 16-byte record exchanged between ranks (row a4/a5)
+  uint32_t keybits; // (!forced) << 31 | fp32 bits of the key
+  uint32_t arrival;
+  uint32_t kv;
+  uint32_t gid;     // (id_base + slot) & 0x7FFFFFFF | running << 31
+};
+
+// Constants uploaded once at create (device copies).
+struct HeadConsts {
+  float m[kMaxBins];        // bin midpoints m_i
+  float log_stay[kMaxBins]; // log(1 - 1/w_i)          (T_ii, D-1)
+  float log_move[kMaxBins]; // log(1/w_{i+1}), -inf at i = k-1  (T_{i,i+1})
+  float log_prior[kMaxBins];// log pi_i
+  uint32_t thr_tab[kMaxBins];// floor(c * m_i) (fp64 on host), 0xFFFFFFFF for c = inf
+  float prior_L;            // E_pi[L] (D-24)
+  int k;
+  int H;
+};
+
+struct Ctx {
+  trail_config cfg;
+  int device = 0;
+  int d = 0, H = 0, k = 0, dtype = 0;
+  size_t esize = 2;            // bytes per W1/embedding element
+  // weights
+  void *w1 = nullptr;          // [H][d] dtype
+  float *b1 = nullptr, *w2 = nullptr, *b2 = nullptr;
+  HeadConsts *consts = nullptr;   // device
+  HeadConsts host_consts;
+  // state
+  float *lq = nullptr;         // [max_slots][k]
+  SlotMeta *meta = nullptr;    // [max_slots]
+  uint32_t *dev_err = nullptr; // sticky bits
+  // workspaces
+  void *xs = nullptr;          // [max_requests][d] staged embeddings (dtype)
+  float *partial = nullptr;    // [S][n][H] layer-1 split-K partials
+  size_t partial_elems = 0;
+  Record *rec_local = nullptr; // [max_sched]
+  Record *rec_all = nullptr;   // [max_sched * world]
+  void *sel_scratch = nullptr; // global scratch for large selections
+  size_t sel_scratch_bytes = 0;
+  // TMA descriptors (bf16 path)
+  CUtensorMap tmap_x, tmap_w128, tmap_w256;
+  bool have_tmaps = false;
+  int num_sms = 148;
+  // NCCL
+  void *nccl_comm = nullptr;
+  int rank = 0, world = 1;
+  // profiling
+  bool prof = false;
+  int prof_n = 0;
+  cudaEvent_t *prof_ev = nullptr;   // pairs
+  int *prof_kid = nullptr;
+  int prof_cap = 0;
+  double prof_ms[TRAIL_K_COUNT] = {0};
+  int64_t prof_cnt[TRAIL_K_COUNT] = {0};
+  // mode 2 (graph-friendly): one fixed event pair per kernel id, re-recorded every launch
+  // (also by CUDA-graph event-record nodes captured while profiling)
+  int prof_mode = 0;
+  cudaEvent_t last_ev[TRAIL_K_COUNT][2] = {};
+  bool last_used[TRAIL_K_COUNT] = {};
+};
+
+// ---------------------------------------------------------------- launchers (host)
+cudaError_t launch_pool(const Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
+                        cudaStream_t s);
+cudaError_t launch_gemv_l1(const Ctx &c, int n, int splits, cudaStream_t s);
+cudaError_t launch_umma_l1(const Ctx &c, int n, int bn, int splits, cudaStream_t s);
+cudaError_t launch_head(const Ctx &c, int n, int splits, const uint32_t *ids,
+                        const uint8_t *is_prefill, const float *prior_override,
+                        float *post, float *L, cudaStream_t s);
+cudaError_t launch_pack(const Ctx &c, const uint32_t *ids, const uint32_t *arrival,
+                        const int32_t *kv, const uint8_t *running, int n, Record *out,
+                        int n_pad_to, cudaStream_t s);
+cudaError_t launch_select(const Ctx &c, const Record *rec, int n, int64_t budget, int max_run,
+                          uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
+                          cudaStream_t s);
+cudaError_t launch_release(const Ctx &c, const uint32_t *ids, int n, cudaStream_t s);
+cudaError_t launch_read_state(const Ctx &c, const uint32_t *ids, int n, float *L, uint32_t *age,
+                              uint32_t *thr, uint8_t *seen, float *post, cudaStream_t s);
+cudaError_t umma_prepare(Ctx &c);                // encode tensor maps, set smem attributes
+int umma_max_bn(const Ctx &c);
+cudaError_t select_prepare(Ctx &c);
+cudaError_t head_prepare(Ctx &c);
+size_t select_scratch_bytes(int n_max);
+int select_smem_capacity();
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+}  // namespace trail
