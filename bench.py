@@ -366,10 +366,9 @@ def run_e2e(args, cfg, t, batches, stream, flush, torch, device, world):
         for k, v in h.items():
             if isinstance(v, torch.Tensor):
                 dv = dbuf[k][: v.numel()]
-                dv.copy_(v, non_blocking=True)
+                dv.copy_(v.reshape(-1), non_blocking=True)
                 views[k] = dv.view(v.shape)
-        t.predict(views["emb"].view(-1, cfg["d"]) if cfg["dtype"] == "f32" else views["emb"],
-                  views["off"], views["ids"], views["pref"], stream=stream)
+        t.predict(views["emb"], views["off"], views["ids"], views["pref"], stream=stream)
         t.schedule(views["sids"], views["arr"], views["kv"], views["run"], h["budget"],
                    stream=stream)
         lists_dev[:cap].copy_(t.run_ids)

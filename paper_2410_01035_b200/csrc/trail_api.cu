@@ -36,12 +36,18 @@ struct ProfScope {
   int slot = -1;
   cudaStream_t s;
   int kid_ = -1;
+  unsigned flags_ = 0;
   ProfScope(Ctx &c_, int kid, cudaStream_t s_) : c(c_), s(s_) {
     if (!c.prof) return;
     if (c.prof_mode == 2) {
       kid_ = kid;
       c.last_used[kid] = true;
-      cudaEventRecord(c.last_ev[kid][0], s);
+      // while a graph is being captured, record as an external event node so every
+      // replay re-records the event; outside capture a plain record
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(s, &cs);
+      flags_ = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+      cudaEventRecordWithFlags(c.last_ev[kid][0], s, flags_);
     } else if (c.prof_n < c.prof_cap) {
       slot = c.prof_n++;
       c.prof_kid[slot] = kid;
@@ -49,7 +55,7 @@ struct ProfScope {
     }
   }
   ~ProfScope() {
-    if (kid_ >= 0) cudaEventRecord(c.last_ev[kid_][1], s);
+    if (kid_ >= 0) cudaEventRecordWithFlags(c.last_ev[kid_][1], s, flags_);
     else if (slot >= 0) cudaEventRecord(c.prof_ev[2 * slot + 1], s);
   }
 };
@@ -269,7 +275,7 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
   ALLOC(c.partial, c.partial_elems * sizeof(float));
   const int max_sched = std::max(1, g.max_sched);
   ALLOC(c.rec_local, (size_t)max_sched * sizeof(Record));
-  if (c.world > 1) ALLOC(c.rec_all, (size_t)max_sched * c.world * sizeof(Record));
+  ALLOC(c.rec_all, (size_t)max_sched * c.world * sizeof(Record));
   c.sel_scratch_bytes = select_scratch_bytes(max_sched * c.world);
   if (c.sel_scratch_bytes) ALLOC(c.sel_scratch, c.sel_scratch_bytes);
 #undef ALLOC
@@ -402,7 +408,7 @@ trail_status trail_schedule_step(trail_handle h, const uint32_t *request_ids,
   if (c.world > 1 && !c.nccl_comm) return TRAIL_ERR_STATE;
   if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
   cudaStream_t s = (cudaStream_t)stream;
-  const int npad = c.world > 1 ? std::max(1, c.cfg.max_sched) : n;
+  const int npad = c.nccl_comm ? std::max(1, c.cfg.max_sched) : n;
   {
     ProfScope p(c, TRAIL_K_PACK, s);
     TRAIL_CUDA(launch_pack(c, request_ids, arrival_seq, kv_blocks, is_running, n, c.rec_local,
@@ -410,7 +416,7 @@ trail_status trail_schedule_step(trail_handle h, const uint32_t *request_ids,
   }
   const Record *sel_in = c.rec_local;
   int total = n;
-  if (c.world > 1) {
+  if (c.nccl_comm) {
     NcclApi &api = nccl();
     ProfScope p(c, TRAIL_K_GATHER, s);
     ncclResult_t r = api.allGather(c.rec_local, c.rec_all, (size_t)npad * sizeof(Record),
