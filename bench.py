@@ -87,6 +87,11 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first_sample(self, timeout: float = 5.0):
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
     def __exit__(self, *a):
         if self.proc:
             self.proc.terminate()
@@ -116,15 +121,18 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- workload
 def make_batches(cfg, nb: int, rank: int, world: int, seed: int):
-    """nb consecutive iterations of the scripted engine (open loop): burst prefill first,
-    then decode with Alpaca-like completions/arrivals."""
+    """The scripted engine (open loop): an initial burst prefill (P:570 shape: every
+    request pools its prompt) that initialises the slots, then nb consecutive steady-state
+    iterations (decode + the Alpaca-like trickle of completions/arrivals) that are timed."""
     eng = W.EngineScript(cfg["n"], cfg["waiting"], d=cfg["d"], dtype=cfg["dtype"],
                          seed=seed + 1000 * rank, arrival_base=rank, arrival_stride=world)
+    init = eng.batch()
+    eng.advance()
     batches = []
     for _ in range(nb):
         batches.append(eng.batch())
         eng.advance()
-    return eng, batches
+    return eng, init, batches
 
 
 def to_dev(a, torch, device):
@@ -157,7 +165,7 @@ def run_ours(args, cfg):
     hbm, tf_burst, tf_sust, peak_src = peaks()
 
     nb = max(1, min(args.distinct, args.steps + args.warmup))
-    eng, batches = make_batches(cfg, nb, rank, world, args.seed)
+    eng, init, batches = make_batches(cfg, nb, rank, world, args.seed)
     w = W.make_weights(cfg["d"], cfg["H"], cfg["k"], cfg["dtype"],
                        edges=W.paper_bin_edges(cfg["k"], cfg["total"]), seed=args.seed)
     max_slots = eng.max_slots
@@ -169,22 +177,29 @@ def run_ours(args, cfg):
         trail_comm_init(t.h, uid[0], rank, world)
 
     # device-resident inputs for every distinct iteration
-    dev = [dict(emb=to_dev(b.emb, torch, device), off=to_dev(b.row_offsets, torch, device),
-                ids=to_dev(b.request_ids, torch, device), pref=to_dev(b.is_prefill, torch, device),
-                sids=to_dev(b.sched_ids, torch, device), arr=to_dev(b.arrival_seq, torch, device),
-                kv=to_dev(b.kv_blocks, torch, device), run=to_dev(b.is_running, torch, device),
-                budget=b.kv_budget, n=b.n, m=b.m, rows=int(b.row_offsets[-1]))
-           for b in batches]
+    def mk(b):
+        return dict(emb=to_dev(b.emb, torch, device), off=to_dev(b.row_offsets, torch, device),
+                    ids=to_dev(b.request_ids, torch, device),
+                    pref=to_dev(b.is_prefill, torch, device),
+                    sids=to_dev(b.sched_ids, torch, device),
+                    arr=to_dev(b.arrival_seq, torch, device),
+                    kv=to_dev(b.kv_blocks, torch, device), run=to_dev(b.is_running, torch, device),
+                    budget=b.kv_budget, n=b.n, m=b.m, rows=int(b.row_offsets[-1]))
+    dev = [mk(b) for b in batches]
+    dev_init = mk(init)
     stream = torch.cuda.Stream(device)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
 
-    def step(i):
-        x = dev[i % nb]
+    def step_x(x):
         t.predict(x["emb"], x["off"], x["ids"], x["pref"], stream=stream)
         t.schedule(x["sids"], x["arr"], x["kv"], x["run"], x["budget"], stream=stream)
 
-    # first pass over the distinct batches eagerly: burst prefill initialises the slots
+    def step(i):
+        step_x(dev[i % nb])
+
+    # burst prefill (initialises every slot), then one eager pass over the cycled batches
     with torch.cuda.stream(stream):
+        step_x(dev_init)
         for i in range(nb):
             step(i)
     torch.cuda.synchronize()
@@ -221,6 +236,7 @@ def run_ours(args, cfg):
           for _ in range(args.steps)]
     kern_ms = {k: [] for k in kernels}
     with ClockSampler(local) as clk:
+        clk.wait_first_sample()
         for i in range(args.steps):
             if not args.no_flush:
                 with torch.cuda.stream(stream):
@@ -282,6 +298,30 @@ def run_ours(args, cfg):
                      "kernel_us": {k: round(v * 1e3, 3) for k, v in avg.items()},
                      "share_of_step": avg[dom] / ms_per_step})
 
+    # ---- burst prefill (P:570 shape): every request mean-pools its prompt rows (K1 streams
+    # ~(rows + n) * d * eb bytes); reported beside the steady-state step, not in `value`
+    burst = None
+    if not args.no_burst:
+        bt = []
+        for _ in range(5):
+            a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                a.record(stream)
+                step_x(dev_init)
+                b2.record(stream)
+            stream.synchronize()
+            pool_ms, _ = trail_profile_read(t.h, "pool")
+            bt.append((a.elapsed_time(b2), pool_ms))
+        eb = 2 if cfg["dtype"] == "bf16" else 4
+        byts = (dev_init["rows"] + dev_init["n"]) * cfg["d"] * eb
+        pool_ms = statistics.median(x[1] for x in bt)
+        burst = {"requests": dev_init["n"], "prompt_rows": dev_init["rows"],
+                 "step_us": statistics.median(x[0] for x in bt) * 1e3,
+                 "pool_us": pool_ms * 1e3, "pool_bytes": byts,
+                 "pool_GBps": byts / (pool_ms / 1e3) / 1e9,
+                 "pool_frac_of_hbm": byts / (pool_ms / 1e3) / 1e9 / hbm}
+
     # ---- end to end through the C ABI with HOST buffers (pinned), copies in the timed region
     e2e = run_e2e(args, cfg, t, batches, stream, flush, torch, device, world)
 
@@ -321,6 +361,7 @@ def run_ours(args, cfg):
                                 if world > 1 else ""),
             },
             "roofline": roof,
+            "burst_prefill": burst,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,
@@ -423,15 +464,20 @@ def _threads():
 
 def oracle_steps(cfg, args, seconds: float, max_steps: int):
     from oracle import trail_ref as R
-    eng, batches = make_batches(cfg, max_steps, 0, 1, args.seed)
+    nb = max(1, min(args.distinct, max_steps))
+    eng, init, batches = make_batches(cfg, nb, 0, 1, args.seed)
     w = W.make_weights(cfg["d"], cfg["H"], cfg["k"], cfg["dtype"],
                        edges=W.paper_bin_edges(cfg["k"], cfg["total"]), seed=args.seed)
     o = R.TrailOracle(W.decode(w["W1"], cfg["dtype"]), w["b1"], w["W2"], w["b2"], w["edges"],
                       cfg["c"], eng.max_slots, x_dtype=cfg["dtype"])
+    o.predict_step(W.decode(init.emb, cfg["dtype"]), init.row_offsets, init.request_ids,
+                   init.is_prefill)                      # burst prefill, untimed
     emb64 = [W.decode(b.emb, cfg["dtype"]) for b in batches]
     times, reqs = [], 0
     t_start = time.perf_counter()
-    for i, b in enumerate(batches):
+    for s in range(max_steps):
+        i = s % nb
+        b = batches[i]
         t0 = time.perf_counter()
         o.predict_step(emb64[i], b.row_offsets, b.request_ids, b.is_prefill)
         o.schedule_step(b.sched_ids, b.arrival_seq, b.kv_blocks, b.is_running, b.kv_budget)
@@ -443,7 +489,7 @@ def oracle_steps(cfg, args, seconds: float, max_steps: int):
 
 
 def cpu_baseline(cfg, args):
-    times, reqs = oracle_steps(cfg, args, seconds=args.cpu_seconds, max_steps=64)
+    times, reqs = oracle_steps(cfg, args, seconds=args.cpu_seconds, max_steps=10_000)
     tot = sum(times)
     return {"value": reqs / tot, "unit": "requests/s", "cores": _threads(), "kind": "oracle",
             "ms_per_step": 1e3 * tot / len(times),
@@ -491,6 +537,7 @@ def main():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-burst", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -158,9 +158,10 @@ cudaError_t launch_head(const Ctx &c, int n, int splits, const uint32_t *ids,
                         const uint8_t *is_prefill, const float *prior_override, float *post,
                         float *L, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  const int warps = 8;
+  // 4 requests per CTA: >= one CTA per SM already at n = 512 (latency-bound kernel)
+  const int warps = 4;
   int blocks = (n + warps - 1) / warps;
-  const int cap = c.num_sms * 4;
+  const int cap = c.num_sms * 8;
   if (blocks > cap) blocks = cap;
   const size_t smem = (size_t)c.k * c.H * sizeof(float);
 #define TRAIL_HEAD(HC)                                                                        \

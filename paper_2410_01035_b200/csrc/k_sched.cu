@@ -129,7 +129,7 @@ __device__ __forceinline__ void block_scan3(SelShared &sh, long long v, int c1, 
 }  // namespace
 
 __global__ void __launch_bounds__(kSelThreads, 1)
-trail_select_kernel(const Record *__restrict__ rec, int n, int npow2, long long budget,
+trail_select_large_kernel(const Record *__restrict__ rec, int n, int npow2, long long budget,
                     int max_run, unsigned long long *gkeys, uint32_t *gidx,
                     uint32_t *__restrict__ run_ids, uint32_t *__restrict__ pre_ids,
                     uint32_t *__restrict__ adm_ids, int32_t *__restrict__ counts) {
@@ -266,13 +266,18 @@ size_t select_scratch_bytes(int n_max) {
 
 cudaError_t select_prepare(Ctx &c) {
   (void)c;
-  return cudaFuncSetAttribute(trail_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = select_fast_prepare();
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(trail_select_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               kSmemCapRecords * 12);
 }
 
 cudaError_t launch_select(const Ctx &c, const Record *rec, int n, int64_t budget, int max_run,
                           uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
                           cudaStream_t s) {
+  if (n <= select_fast_capacity())
+    return launch_select_fast(c, rec, nullptr, nullptr, nullptr, nullptr, nullptr, n, budget,
+                              max_run, run, pre, adm, counts, s);
   int p = 1;
   while (p < n) p <<= 1;
   if (p < 2) p = 2;
@@ -285,7 +290,7 @@ cudaError_t launch_select(const Ctx &c, const Record *rec, int n, int64_t budget
     gi = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(c.sel_scratch) + (size_t)p * 8);
     smem = 0;
   }
-  trail_select_kernel<<<1, kSelThreads, smem, s>>>(rec, n, p, (long long)budget, max_run, gk, gi,
+  trail_select_large_kernel<<<1, kSelThreads, smem, s>>>(rec, n, p, (long long)budget, max_run, gk, gi,
                                                    run, pre, adm, counts);
   return cudaGetLastError();
 }

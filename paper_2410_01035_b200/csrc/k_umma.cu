@@ -185,19 +185,30 @@ trail_umma_l1_kernel(const __grid_constant__ CUtensorMap tmap_x,
   mbar_wait(done, 0);
   __syncwarp();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int row = m0 + warp * 32 + lane;
-  float *dst = partial + ((int64_t)s * n + row) * H + n0;
+  // Stage each warp's 32 rows through (now idle) pipeline shared memory, then write them
+  // out row by row: one 16-byte vector per lane, BN*4 contiguous bytes per row (coalesced).
+  constexpr int LD = BN + 4;                       // padded row stride (floats)
+  float *stile = reinterpret_cast<float *>(smem) + warp * 32 * LD;
 #pragma unroll 1
   for (int c = 0; c < BN; c += 32) {
     uint32_t r[32];
     tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, r);
-    if (row < n) {
-      float4 *d4 = reinterpret_cast<float4 *>(dst + c);
+    float4 *srow = reinterpret_cast<float4 *>(stile + lane * LD + c);
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        d4[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+    for (int q = 0; q < 8; ++q)
+      srow[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                             __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-    }
+  }
+  __syncwarp();
+  const int row0 = m0 + warp * 32;
+#pragma unroll 4
+  for (int rr = 0; rr < 32; ++rr) {
+    if (row0 + rr >= n) break;
+    float *dst = partial + ((int64_t)s * n + row0 + rr) * H + n0;
+    const float *src = stile + rr * LD;
+#pragma unroll
+    for (int c = lane * 4; c < BN; c += 128)
+      *reinterpret_cast<float4 *>(dst + c) = *reinterpret_cast<const float4 *>(src + c);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

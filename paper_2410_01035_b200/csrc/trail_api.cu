@@ -408,6 +408,14 @@ trail_status trail_schedule_step(trail_handle h, const uint32_t *request_ids,
   if (c.world > 1 && !c.nccl_comm) return TRAIL_ERR_STATE;
   if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
   cudaStream_t s = (cudaStream_t)stream;
+  if (!c.nccl_comm && n <= select_fast_capacity()) {
+    // local selection: the record build is fused into the selection kernel
+    ProfScope p(c, TRAIL_K_SELECT, s);
+    TRAIL_CUDA(launch_select_fast(c, nullptr, c.rec_local, request_ids, arrival_seq, kv_blocks,
+                                  is_running, n, kv_budget, max_run, run_ids, preempt_ids,
+                                  admit_ids, counts, s));
+    return TRAIL_OK;
+  }
   const int npad = c.nccl_comm ? std::max(1, c.cfg.max_sched) : n;
   {
     ProfScope p(c, TRAIL_K_PACK, s);

@@ -107,6 +107,15 @@ cudaError_t launch_read_state(const Ctx &c, const uint32_t *ids, int n, float *L
 cudaError_t umma_prepare(Ctx &c);                // encode tensor maps, set smem attributes
 int umma_max_bn(const Ctx &c);
 cudaError_t select_prepare(Ctx &c);
+cudaError_t select_fast_prepare();
+int select_fast_capacity();
+// rec_in != nullptr: select over given records; else build local records (fused pack)
+// from (ids, arrival, kv, running) into rec_out and select over them.
+cudaError_t launch_select_fast(const Ctx &c, const Record *rec_in, Record *rec_out,
+                               const uint32_t *ids, const uint32_t *arrival, const int32_t *kv,
+                               const uint8_t *running, int n, int64_t budget, int max_run,
+                               uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
+                               cudaStream_t s);
 cudaError_t head_prepare(Ctx &c);
 size_t select_scratch_bytes(int n_max);
 int select_smem_capacity();
