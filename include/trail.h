@@ -53,9 +53,12 @@ typedef enum { TRAIL_F32 = 0, TRAIL_BF16 = 1 } trail_dtype;
 
 /* Layer-1 kernel selection (row a2). */
 typedef enum {
-  TRAIL_L1_AUTO = 0,   /* GEMV for fp32 or small n, tcgen05 GEMM otherwise */
-  TRAIL_L1_GEMV = 1,   /* K2a: warp-per-output-slice split-K GEMV (CUDA cores) */
-  TRAIL_L1_UMMA = 2    /* K2b: TMA-fed tcgen05/TMEM GEMM (bf16 only) */
+  TRAIL_L1_AUTO = 0,   /* GEMV for fp32 or small n, fused tcgen05 kernel otherwise */
+  TRAIL_L1_GEMV = 1,   /* K2a: warp-per-output-slice split-K GEMV (CUDA cores) + head K3 */
+  TRAIL_L1_UMMA = 2,   /* K2c: fused TMA + tcgen05/TMEM layer 1, cluster split-K reduction,
+                          layer 2 and head in the epilogue (bf16 only) */
+  TRAIL_L1_UMMA_UNFUSED = 3  /* K2b + K3: tcgen05 layer 1 with split-K partials in global
+                                memory, then the separate head kernel (bf16 only) */
 } trail_l1_mode;
 
 /* Sticky device-side error bits (trail_device_errors). */
@@ -206,7 +209,7 @@ TRAIL_API trail_status trail_profile_enable(trail_handle h, int32_t enable);
 TRAIL_API trail_status trail_profile_read(trail_handle h, int32_t kid, double *total_ms,
                                 int64_t *launches, int32_t reset);
 
-/* Overrides cfg.l1_mode for subsequent calls (TRAIL_L1_UMMA requires bf16). */
+/* Overrides cfg.l1_mode for subsequent calls (the tcgen05 modes require bf16). */
 TRAIL_API trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode);
 
 /* Which layer-1 kernel trail_predict_step uses for n requests, and its split-K factor. */

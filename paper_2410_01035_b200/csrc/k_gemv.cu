@@ -55,6 +55,8 @@ __global__ void __launch_bounds__(kWarps * 32)
 trail_gemv_l1_kernel(const T *__restrict__ w1, const T *__restrict__ xs, int n, int d, int H,
                      int kchunk, float *__restrict__ partial) {
   constexpr int VEC = V16<T>::N;
+  griddep_wait();
+  griddep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int o0 = blockIdx.x * kRowsPerCta + warp * kRowsPerWarp;
   const int s = blockIdx.y;
@@ -108,13 +110,11 @@ cudaError_t launch_gemv_l1(const Ctx &c, int n, int splits, cudaStream_t s) {
   kchunk = (kchunk + vec - 1) / vec * vec;
   dim3 grid(c.H / kRowsPerCta, splits);
   if (c.dtype == TRAIL_BF16)
-    trail_gemv_l1_kernel<__nv_bfloat16><<<grid, kWarps * 32, 0, s>>>(
-        (const __nv_bfloat16 *)c.w1, (const __nv_bfloat16 *)c.xs, n, c.d, c.H, kchunk,
-        c.partial);
-  else
-    trail_gemv_l1_kernel<float><<<grid, kWarps * 32, 0, s>>>(
-        (const float *)c.w1, (const float *)c.xs, n, c.d, c.H, kchunk, c.partial);
-  return cudaGetLastError();
+    return launch_k(trail_gemv_l1_kernel<__nv_bfloat16>, grid, dim3(kWarps * 32), 0, s,
+                    (const __nv_bfloat16 *)c.w1, (const __nv_bfloat16 *)c.xs, n, c.d, c.H, kchunk,
+                    c.partial);
+  return launch_k(trail_gemv_l1_kernel<float>, grid, dim3(kWarps * 32), 0, s, (const float *)c.w1,
+                  (const float *)c.xs, n, c.d, c.H, kchunk, c.partial);
 }
 
 }  // namespace trail

@@ -47,6 +47,8 @@ trail_head_kernel(const float *__restrict__ partial, int splits, int n,
   for (int i = threadIdx.x; i < k * H / 4; i += blockDim.x)
     reinterpret_cast<float4 *>(w2s)[i] = __ldg(reinterpret_cast<const float4 *>(w2) + i);
   __syncthreads();
+  griddep_wait();      // partials from layer 1, slot state from the previous step
+  griddep_launch();
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool active = lane < k;
@@ -165,17 +167,16 @@ cudaError_t launch_head(const Ctx &c, int n, int splits, const uint32_t *ids,
   if (blocks > cap) blocks = cap;
   const size_t smem = (size_t)c.k * c.H * sizeof(float);
 #define TRAIL_HEAD(HC)                                                                        \
-  trail_head_kernel<HC><<<blocks, warps * 32, smem, s>>>(                                     \
-      c.partial, splits, n, c.b1, c.w2, c.b2, c.consts, ids, is_prefill, prior_override,      \
-      c.cfg.max_slots, c.lq, c.meta, post, L, c.dev_err)
+  return launch_k(trail_head_kernel<HC>, dim3(blocks), dim3(warps * 32), smem, s, c.partial,  \
+                  splits, n, c.b1, c.w2, c.b2, c.consts, ids, is_prefill, prior_override,     \
+                  c.cfg.max_slots, c.lq, c.meta, post, L, c.dev_err)
   switch (c.H / 128) {
-    case 1: TRAIL_HEAD(1); break;
-    case 2: TRAIL_HEAD(2); break;
-    case 3: TRAIL_HEAD(3); break;
-    default: TRAIL_HEAD(4); break;
+    case 1: TRAIL_HEAD(1);
+    case 2: TRAIL_HEAD(2);
+    case 3: TRAIL_HEAD(3);
+    default: TRAIL_HEAD(4);
   }
 #undef TRAIL_HEAD
-  return cudaGetLastError();
 }
 
 cudaError_t head_prepare(Ctx &c) {

@@ -27,6 +27,8 @@ __global__ void trail_pack_kernel(const uint32_t *__restrict__ ids,
                                   const HeadConsts *__restrict__ cst, int n, int n_pad_to,
                                   int max_slots, uint32_t id_base, Record *__restrict__ out,
                                   uint32_t *__restrict__ err) {
+  griddep_wait();
+  griddep_launch();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_pad_to) return;
   Record r;
@@ -133,6 +135,8 @@ trail_select_large_kernel(const Record *__restrict__ rec, int n, int npow2, long
                     int max_run, unsigned long long *gkeys, uint32_t *gidx,
                     uint32_t *__restrict__ run_ids, uint32_t *__restrict__ pre_ids,
                     uint32_t *__restrict__ adm_ids, int32_t *__restrict__ counts) {
+  griddep_wait();
+  griddep_launch();
   extern __shared__ __align__(16) uint8_t sel_smem[];
   __shared__ SelShared sh;
   __shared__ int s_valid;
@@ -267,6 +271,7 @@ size_t select_scratch_bytes(int n_max) {
 cudaError_t select_prepare(Ctx &c) {
   (void)c;
   cudaError_t e = select_fast_prepare();
+  if (e == cudaSuccess) e = select_radix_prepare();
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(trail_select_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               kSmemCapRecords * 12);
@@ -275,6 +280,9 @@ cudaError_t select_prepare(Ctx &c) {
 cudaError_t launch_select(const Ctx &c, const Record *rec, int n, int64_t budget, int max_run,
                           uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
                           cudaStream_t s) {
+  if (!use_bitonic_select() && n <= select_radix_capacity())
+    return launch_select_radix(c, rec, nullptr, nullptr, nullptr, nullptr, nullptr, n, budget,
+                               max_run, run, pre, adm, counts, s);
   if (n <= select_fast_capacity())
     return launch_select_fast(c, rec, nullptr, nullptr, nullptr, nullptr, nullptr, n, budget,
                               max_run, run, pre, adm, counts, s);
@@ -298,6 +306,8 @@ cudaError_t launch_select(const Ctx &c, const Record *rec, int n, int64_t budget
 // ------------------------------------------------------------------ release / read state
 __global__ void trail_release_kernel(const uint32_t *__restrict__ ids, int n, int max_slots,
                                      SlotMeta *__restrict__ meta, uint32_t *__restrict__ err) {
+  griddep_wait();
+  griddep_launch();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t slot = ids[i];
@@ -318,6 +328,8 @@ __global__ void trail_read_state_kernel(const uint32_t *__restrict__ ids, int n,
                                         int max_slots, const SlotMeta *__restrict__ meta,
                                         const float *__restrict__ lq, float *L, uint32_t *age,
                                         uint32_t *thr, uint8_t *seen, float *post) {
+  griddep_wait();
+  griddep_launch();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t slot = ids[i];

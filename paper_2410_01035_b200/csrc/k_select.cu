@@ -166,6 +166,8 @@ trail_select_kernel(const Record *rec_in, Record *rec_out,
   const int t = threadIdx.x;
   const int lane = t & 31;
   const Record *rec = rec_in ? rec_in : rec_out;
+  griddep_wait();      // slot state written by the head kernel
+  griddep_launch();
 
   // 1. load / build records; composite keys; padding sorts last
   unsigned long long k[E];
@@ -324,20 +326,20 @@ cudaError_t launch_select_fast(const Ctx &c, const Record *rec_in, Record *rec_o
   const int N = std::max(kT, pow2_at_least(std::max(n, 1)));
   const int E = N / kT;
   const size_t smem = (size_t)N * 12;
-#define TRAIL_SEL_LAUNCH(EE)                                                                    \
-  trail_select_kernel<EE><<<1, kT, smem, s>>>(rec_in, rec_out, ids, arrival, kv, running, c.meta, \
-                                             c.consts, c.cfg.max_slots, c.cfg.id_base, c.dev_err, \
-                                             n, (long long)budget, max_run, run, pre, adm, counts)
+#define TRAIL_SEL_LAUNCH(EE)                                                                  \
+  return launch_k(trail_select_kernel<EE>, dim3(1), dim3(kT), smem, s, rec_in, rec_out, ids,   \
+                  arrival, kv, running, (const SlotMeta *)c.meta, (const HeadConsts *)c.consts, \
+                  c.cfg.max_slots, c.cfg.id_base, c.dev_err, n, (long long)budget, max_run, run, \
+                  pre, adm, counts)
   switch (E) {
-    case 1: TRAIL_SEL_LAUNCH(1); break;
-    case 2: TRAIL_SEL_LAUNCH(2); break;
-    case 4: TRAIL_SEL_LAUNCH(4); break;
-    case 8: TRAIL_SEL_LAUNCH(8); break;
-    case 16: TRAIL_SEL_LAUNCH(16); break;
+    case 1: TRAIL_SEL_LAUNCH(1);
+    case 2: TRAIL_SEL_LAUNCH(2);
+    case 4: TRAIL_SEL_LAUNCH(4);
+    case 8: TRAIL_SEL_LAUNCH(8);
+    case 16: TRAIL_SEL_LAUNCH(16);
     default: return cudaErrorInvalidValue;
   }
 #undef TRAIL_SEL_LAUNCH
-  return cudaGetLastError();
 }
 
 }  // namespace trail

@@ -152,6 +152,8 @@ trail_umma_l1_kernel(const __grid_constant__ CUtensorMap tmap_x,
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();      // X is produced by the pool kernel
+  griddep_launch();
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
@@ -274,12 +276,10 @@ cudaError_t launch_umma_l1(const Ctx &c, int n, int bn, int splits, cudaStream_t
   const int kblocks = c.d / BK;
   dim3 grid((n + BM - 1) / BM, c.H / bn, splits);
   if (bn == 256)
-    trail_umma_l1_kernel<256><<<grid, 128, UCfg<256>::SMEM, s>>>(c.tmap_x, c.tmap_w256, n, c.H,
-                                                                kblocks, splits, c.partial);
-  else
-    trail_umma_l1_kernel<128><<<grid, 128, UCfg<128>::SMEM, s>>>(c.tmap_x, c.tmap_w128, n, c.H,
-                                                                kblocks, splits, c.partial);
-  return cudaGetLastError();
+    return launch_k(trail_umma_l1_kernel<256>, grid, dim3(128), UCfg<256>::SMEM, s, c.tmap_x,
+                    c.tmap_w256, n, c.H, kblocks, splits, c.partial);
+  return launch_k(trail_umma_l1_kernel<128>, grid, dim3(128), UCfg<128>::SMEM, s, c.tmap_x,
+                  c.tmap_w128, n, c.H, kblocks, splits, c.partial);
 }
 
 }  // namespace trail

@@ -5,6 +5,7 @@
 #include <math.h>
 #include <nccl.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -64,6 +65,12 @@ void plan_l1(const Ctx &c, int n, int *mode, int *bn, int *splits) {
   int m = c.cfg.l1_mode;
   if (c.dtype == TRAIL_F32) m = TRAIL_L1_GEMV;
   else if (m == TRAIL_L1_AUTO) m = (n <= kGemvMaxN) ? TRAIL_L1_GEMV : TRAIL_L1_UMMA;
+  if (m == TRAIL_L1_UMMA) {
+    *mode = TRAIL_L1_UMMA;
+    *bn = 128;
+    *splits = fused_splits(c, n);
+    return;
+  }
   if (m == TRAIL_L1_GEMV) {
     const int ctas_x = c.H / 16;
     const int vec = c.dtype == TRAIL_BF16 ? 8 : 4;
@@ -76,7 +83,7 @@ void plan_l1(const Ctx &c, int n, int *mode, int *bn, int *splits) {
     const int b = (n > 1024 && umma_max_bn(c) == 256) ? 256 : 128;
     const int tiles = ((n + 127) / 128) * (c.H / b);
     const int kblocks = c.d / 64;
-    *mode = TRAIL_L1_UMMA;
+    *mode = TRAIL_L1_UMMA_UNFUSED;
     *bn = b;
     *splits = std::max(1, std::min(kblocks, c.num_sms / std::max(1, tiles)));
   }
@@ -125,7 +132,7 @@ trail_status set_device(const Ctx &c) {
 
 void free_ctx(Ctx &c) {
   void *ptrs[] = {c.w1, c.b1, c.w2, c.b2, c.consts, c.lq, c.meta, c.dev_err, c.xs,
-                  c.partial, c.rec_local, c.rec_all, c.sel_scratch};
+                  c.partial, c.rec_local, c.rec_all, c.sel_scratch, c.zpart, c.arrive_cnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c.prof_ev) {
@@ -145,7 +152,7 @@ size_t partial_elems_needed(const Ctx &c) {
     for (int forced = 0; forced < 2; ++forced) {
       Ctx tmp_c;
       tmp_c.cfg = c.cfg;
-      tmp_c.cfg.l1_mode = forced ? TRAIL_L1_GEMV : TRAIL_L1_UMMA;
+      tmp_c.cfg.l1_mode = forced ? TRAIL_L1_GEMV : TRAIL_L1_UMMA_UNFUSED;
       if (c.dtype == TRAIL_F32 && !forced) continue;
       tmp_c.d = c.d; tmp_c.H = c.H; tmp_c.dtype = c.dtype; tmp_c.num_sms = c.num_sms;
       int mode, bn, s;
@@ -190,8 +197,8 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
   if (!(g.c >= 0.0)) return TRAIL_ERR_INVALID;   // rejects NaN and negatives
   if (g.max_slots <= 0 || g.max_requests <= 0 || g.max_sched < 0) return TRAIL_ERR_INVALID;
   if (g.world_size < 1) return TRAIL_ERR_INVALID;
-  if (g.l1_mode < 0 || g.l1_mode > 2) return TRAIL_ERR_INVALID;
-  if (g.l1_mode == TRAIL_L1_UMMA && g.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
+  if (g.l1_mode < 0 || g.l1_mode > 3) return TRAIL_ERR_INVALID;
+  if (g.l1_mode >= TRAIL_L1_UMMA && g.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
   if ((int64_t)g.max_sched * g.world_size > (1 << 26)) return TRAIL_ERR_INVALID;
   const int k = g.k;
   const double *e = g.bin_edges;
@@ -278,6 +285,13 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
   ALLOC(c.rec_all, (size_t)max_sched * c.world * sizeof(Record));
   c.sel_scratch_bytes = select_scratch_bytes(max_sched * c.world);
   if (c.sel_scratch_bytes) ALLOC(c.sel_scratch, c.sel_scratch_bytes);
+  const size_t m_tiles = ((size_t)g.max_requests + 127) / 128;
+  if (c.dtype == TRAIL_BF16) {
+    ALLOC(c.zpart, (size_t)g.max_requests * (c.H / 128) * k * sizeof(float));
+    ALLOC(c.arrive_cnt, m_tiles * 16 * sizeof(uint32_t));
+    if (cudaMemset(c.arrive_cnt, 0, m_tiles * 16 * sizeof(uint32_t)) != cudaSuccess)
+      return fail(TRAIL_ERR_CUDA);
+  }
 #undef ALLOC
   if (cudaMemcpy(c.w1, g.w1, w1_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(c.b1, g.b1, c.H * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -290,7 +304,7 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
       cudaMemset(c.xs, 0, (size_t)g.max_requests * c.d * c.esize) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
   if (umma_prepare(c) != cudaSuccess || head_prepare(c) != cudaSuccess ||
-      select_prepare(c) != cudaSuccess)
+      fused_prepare(c) != cudaSuccess || select_prepare(c) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(TRAIL_ERR_CUDA);
   *out = h;
@@ -307,8 +321,8 @@ trail_status trail_destroy(trail_handle h) {
 }
 
 trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode) {
-  if (!h || l1_mode < 0 || l1_mode > 2) return TRAIL_ERR_INVALID;
-  if (l1_mode == TRAIL_L1_UMMA && h->c.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
+  if (!h || l1_mode < 0 || l1_mode > 3) return TRAIL_ERR_INVALID;
+  if (l1_mode >= TRAIL_L1_UMMA && h->c.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
   h->c.cfg.l1_mode = l1_mode;
   return TRAIL_OK;
 }
@@ -339,10 +353,17 @@ trail_status trail_predict_step(trail_handle h, const void *emb, int64_t emb_ld,
   cudaStream_t s = (cudaStream_t)stream;
   int mode, bn, splits;
   plan_l1(c, n, &mode, &bn, &splits);
-  if ((size_t)splits * n * c.H > c.partial_elems) return TRAIL_ERR_CAPACITY;
+  if (mode != TRAIL_L1_UMMA && (size_t)splits * n * c.H > c.partial_elems)
+    return TRAIL_ERR_CAPACITY;
   {
     ProfScope p(c, TRAIL_K_POOL, s);
     TRAIL_CUDA(launch_pool(c, emb, emb_ld, row_offsets, n, s));
+  }
+  if (mode == TRAIL_L1_UMMA) {   // layer 1 + layer 2 + head in one kernel
+    ProfScope p(c, TRAIL_K_UMMA, s);
+    TRAIL_CUDA(launch_fused_predict(c, n, splits, request_ids, is_prefill, prior_override,
+                                    posteriors, expected_remaining, s));
+    return TRAIL_OK;
   }
   if (mode == TRAIL_L1_GEMV) {
     ProfScope p(c, TRAIL_K_GEMV, s);
@@ -408,12 +429,17 @@ trail_status trail_schedule_step(trail_handle h, const uint32_t *request_ids,
   if (c.world > 1 && !c.nccl_comm) return TRAIL_ERR_STATE;
   if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
   cudaStream_t s = (cudaStream_t)stream;
-  if (!c.nccl_comm && n <= select_fast_capacity()) {
+  if (!c.nccl_comm && n <= select_radix_capacity()) {
     // local selection: the record build is fused into the selection kernel
     ProfScope p(c, TRAIL_K_SELECT, s);
-    TRAIL_CUDA(launch_select_fast(c, nullptr, c.rec_local, request_ids, arrival_seq, kv_blocks,
-                                  is_running, n, kv_budget, max_run, run_ids, preempt_ids,
-                                  admit_ids, counts, s));
+    if (use_bitonic_select())
+      TRAIL_CUDA(launch_select_fast(c, nullptr, c.rec_local, request_ids, arrival_seq, kv_blocks,
+                                    is_running, n, kv_budget, max_run, run_ids, preempt_ids,
+                                    admit_ids, counts, s));
+    else
+      TRAIL_CUDA(launch_select_radix(c, nullptr, c.rec_local, request_ids, arrival_seq,
+                                     kv_blocks, is_running, n, kv_budget, max_run, run_ids,
+                                     preempt_ids, admit_ids, counts, s));
     return TRAIL_OK;
   }
   const int npad = c.nccl_comm ? std::max(1, c.cfg.max_sched) : n;
@@ -567,3 +593,22 @@ trail_status trail_profile_read(trail_handle h, int32_t kid, double *total_ms, i
 }
 
 }  // extern "C"
+
+namespace trail {
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("TRAIL_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+bool use_bitonic_select() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("TRAIL_SELECT");
+    v = (e && e[0] == 'b') ? 1 : 0;
+  }
+  return v == 1;
+}
+}  // namespace trail

@@ -61,6 +61,8 @@ struct Ctx {
   void *xs = nullptr;          // [max_requests][d] staged embeddings (dtype)
   float *partial = nullptr;    // [S][n][H] layer-1 split-K partials
   size_t partial_elems = 0;
+  float *zpart = nullptr;      // [max_requests][H/128][k] fused kernel: layer-2 partial logits
+  uint32_t *arrive_cnt = nullptr;  // [m_tiles][16] fused kernel: column-tile arrival counters
   Record *rec_local = nullptr; // [max_sched]
   Record *rec_all = nullptr;   // [max_sched * world]
   void *sel_scratch = nullptr; // global scratch for large selections
@@ -106,7 +108,20 @@ cudaError_t launch_read_state(const Ctx &c, const uint32_t *ids, int n, float *L
                               uint32_t *thr, uint8_t *seen, float *post, cudaStream_t s);
 cudaError_t umma_prepare(Ctx &c);                // encode tensor maps, set smem attributes
 int umma_max_bn(const Ctx &c);
+cudaError_t fused_prepare(Ctx &c);
+int fused_splits(const Ctx &c, int n);
+cudaError_t launch_fused_predict(const Ctx &c, int n, int splits, const uint32_t *ids,
+                                 const uint8_t *is_prefill, const float *prior_override,
+                                 float *post, float *L, cudaStream_t s);
 cudaError_t select_prepare(Ctx &c);
+cudaError_t select_radix_prepare();
+int select_radix_capacity();
+cudaError_t launch_select_radix(const Ctx &c, const Record *rec_in, Record *rec_out,
+                                const uint32_t *ids, const uint32_t *arrival, const int32_t *kv,
+                                const uint8_t *running, int n, int64_t budget, int max_run,
+                                uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
+                                cudaStream_t s);
+bool use_bitonic_select();
 cudaError_t select_fast_prepare();
 int select_fast_capacity();
 // rec_in != nullptr: select over given records; else build local records (fused pack)
@@ -119,6 +134,37 @@ cudaError_t launch_select_fast(const Ctx &c, const Record *rec_in, Record *rec_o
 cudaError_t head_prepare(Ctx &c);
 size_t select_scratch_bytes(int n_max);
 int select_smem_capacity();
+
+// ---------------------------------------------------------------- launch helper
+// Programmatic dependent launch (PDL): consecutive kernels of a step overlap the next
+// kernel's launch + prologue with the previous kernel's tail.  Every kernel executes
+// griddep_wait() before touching data produced by an earlier kernel and
+// griddep_launch() once all its CTAs are resident (so a waiting dependent can never
+// starve it of SM resources).
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ float warp_sum(float v) {

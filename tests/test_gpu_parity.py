@@ -41,6 +41,10 @@ CASES = [
     ("bf16", 64, 512, 256, 10, 2, 0.0),      # H = 256
     ("bf16", 40, 256, 128, 5, 2, 0.0),       # H = 128, k = 5
     ("bf16", 33, 4096, 384, 32, 2, 0.0),     # H = 384, k = 32 (every lane a bin)
+    ("bf16", 512, 4096, 512, 10, 3, 0.05),   # unfused tcgen05 GEMM + separate head
+    ("bf16", 200, 1024, 256, 20, 3, 0.1),
+    ("bf16", 2000, 512, 512, 10, 2, 0.0),    # fused kernel, no split (S = 1), 16 M tiles
+    ("bf16", 129, 8192, 512, 20, 2, 0.5),    # fused kernel, 16-CTA clusters
     ("f32", 64, 4096, 512, 10, 0, 0.0),      # config 1 shape (fp32 GEMV)
     ("f32", 9, 1024, 256, 3, 1, 1.0),
 ]
@@ -181,11 +185,12 @@ def test_gemv_and_umma_agree():
     n, d = 16, 4096
     w = W.make_weights(d, 512, 10, "bf16", seed=12)
     res = []
-    for mode in (1, 2):
+    for mode in (1, 2, 3):
         t, _ = make_pair(w, 0.8, n, n, n, "bf16", l1_mode=mode)
         emb, off, pref = W.make_step_inputs(n, d, "bf16", prefill_frac=0.0, seed=3)
         res.append(gpu_predict(t, emb, off, np.arange(n, dtype=np.uint32), pref))
     assert np.abs(res[0][0] - res[1][0]).max() < 1e-4
+    assert np.abs(res[0][0] - res[2][0]).max() < 1e-4
 
 
 # ----------------------------------------------------------------------------- selection
