@@ -209,6 +209,15 @@ TRAIL_API trail_status trail_profile_enable(trail_handle h, int32_t enable);
 TRAIL_API trail_status trail_profile_read(trail_handle h, int32_t kid, double *total_ms,
                                 int64_t *launches, int32_t reset);
 
+/* Diagnostics: per-CTA phase timestamps of the fused tcgen05 predict kernel (16 u64 per CTA:
+ * globaltimer ns at entry, after the prologue, first stage landed, mainloop done, tile
+ * staged, cluster barrier passed, reduction done, second barrier passed, exit; [14] = ran the
+ * head, [15] = SM id).  enable allocates room for max_ctas CTAs (0 = off); a launch whose
+ * grid exceeds it is not traced.  trail_trace_read synchronises and copies max_ctas entries
+ * to host memory. */
+TRAIL_API trail_status trail_trace_enable(trail_handle h, int32_t max_ctas);
+TRAIL_API trail_status trail_trace_read(trail_handle h, uint64_t *host_out, int32_t max_ctas);
+
 /* Overrides cfg.l1_mode for subsequent calls (the tcgen05 modes require bf16). */
 TRAIL_API trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode);
 

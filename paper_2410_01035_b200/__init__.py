@@ -27,6 +27,8 @@ from .trail import (  # noqa: F401
     trail_schedule_select,
     trail_schedule_step,
     trail_set_l1_mode,
+    trail_trace_enable,
+    trail_trace_read,
 )
 
 __all__ = [n for n in dir() if n.startswith("trail_")] + ["Trail", "TrailError", "load_library"]

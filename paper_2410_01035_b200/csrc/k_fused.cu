@@ -1,7 +1,7 @@
 // K2c — the fused predict kernel (rows a2 + a3): layer 1 on tcgen05 with a cluster split-K
 // reduction through distributed shared memory, bias + ReLU + layer-2 partial logits in the
 // epilogue, and the head (softmax, Bayesian refinement, expected length, state update) run
-// by the last of the H/128 column-tile clusters to finish each row group.
+// by the last of the H/128 column-tile CTAs to finish each row group.
 //
 //   P:201  h = ReLU(W1 x + b1) (d -> 512), z = W2 h + b2 (512 -> k)
 //   P:204  p = softmax(z) (CrossEntropy-trained logits, reading D-6)
@@ -9,28 +9,38 @@
 //   P:220-222 (D-1, D-2)  q^(t) = normalise((T q^(t-1)) * p^(t)), in the log domain (D-22)
 //   P:226  L_t = sum_i q(i) m_i
 //
-// Grid (m_tiles, H/128, S) with cluster dims (1, 1, S): the S CTAs of a cluster compute the
-// same 128-request x 128-hidden tile over disjoint K ranges.
+// Grid (m_tiles, H/128, S) with cluster dims (1, 1, S), S in [1, 16] chosen on the host so
+// that every cluster is resident in one wave (cudaOccupancyMaxActiveClusters).  The S CTAs of
+// a cluster compute the same 128-request x 128-hidden tile over disjoint K ranges.
 //   warp 0 / lane 0 : TMA producer (X tile 128x64 + W1 tile 128x64 per stage, SW128)
 //   warp 1 / lane 0 : tcgen05.mma.cta_group::1.kind::f16 issuer, accumulator in TMEM
-//   all 4 warps     : epilogue
-//     1. TMEM -> registers -> own shared memory (fp32 128x128 partial tile)
-//     2. cluster barrier; CTA r of the cluster sums rows [r*128/S, (r+1)*128/S) over the S
-//        partial tiles (ld.shared::cluster, fixed order -> deterministic), adds b1, ReLU,
-//        and contracts its 128 hidden units with W2[:, n0:n0+128] -> z_part[row][tile][k]
-//     3. release fence + atomic arrival counter per (m_tile, r); the CTA that completes
-//        the H/128 column tiles of that row group runs the head, one thread per request.
+//   warps 2-7       : stage the W2 / b1 slices of this column tile (overlaps the mainloop)
+//   all 8 warps     : epilogue
+//     1. TMEM -> registers -> own shared memory (fp32 128x128 partial tile, padded rows)
+//     2. cluster barrier; each CTA PUSHES row group r of its tile to CTA r with one bulk
+//        shared::cta -> shared::cluster copy per peer (async engine, completion on the
+//        receiver's mbarrier), so CTA r owns rows [r*128/S, (r+1)*128/S);
+//     3. CTA r sums its rows over the S partials in fixed rank order (deterministic), adds
+//        b1, ReLU, and contracts its 128 hidden units with W2[:, n0:n0+128] -> z_part;
+//     4. release fence + atomic arrival counter per (m_tile, r); the CTA that completes the
+//        H/128 column tiles of that row group runs the head, one thread per request.
 // No fp32 h round trip through HBM and no separate head launch.  KB (template) bounds the
-// bin count so that per-bin loops unroll into registers without code bloat.
+// bin count; W2 rows >= k are zero-padded in shared memory so the layer-2 loops have a
+// compile-time trip count.
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
+#include "sm100_ptx.cuh"
 #include "trail_internal.cuh"
 
 namespace trail {
 
+using namespace ptx;
+
 namespace {
+constexpr int THREADS = 256;
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int BK = 64;
@@ -39,112 +49,24 @@ constexpr int MAXS = 16;                              // max cluster size along 
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int TILE_LD = BN + 4;                       // padded fp32 row stride
-constexpr int PIPE_BYTES = STAGES * STAGE_BYTES;      // 192 KB, reused for the tile
+constexpr int TILE_LD = BN + 4;                       // padded fp32 row stride (528 B)
+constexpr int ROW_BYTES = TILE_LD * 4;
+constexpr int TILE_BYTES = BM * ROW_BYTES;            // 67584
+constexpr int LAND_OFF = TILE_BYTES;                  // landing slots for peers' row groups
+constexpr int PIPE_BYTES = STAGES * STAGE_BYTES;      // 192 KB, reused by tile + landing
 constexpr int BAR_OFF = PIPE_BYTES;
 constexpr int W2_OFF = PIPE_BYTES + 256;
 constexpr int W2_FLOATS = kMaxBins * BN;
-constexpr int SMEM_TOTAL = W2_OFF + (W2_FLOATS + BN) * 4;
-static_assert(BM * TILE_LD * 4 <= PIPE_BYTES, "tile must fit in the pipeline buffers");
+constexpr int SMEM_USED = W2_OFF + (W2_FLOATS + BN) * 4;
+constexpr int SMEM_TOTAL = SMEM_USED + 1024;          // + slack for 1024-byte alignment
+static_assert(LAND_OFF + (BM + MAXS) * ROW_BYTES <= PIPE_BYTES, "tile + landing must fit");
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}\n"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar,
-                                            int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
-  return d;
-}
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(M >> 4) << 24);
-}
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                          uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accum));
-}
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-        "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// address of `local_addr` in the shared memory of cluster CTA `rank` (volatile: it must not
-// be hoisted above the cluster barrier; the loads that use it may then be batched freely)
-__device__ __forceinline__ uint32_t mapa(uint32_t local_addr, uint32_t rank) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
-  return remote;
-}
-__device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr) {
-  float4 v;
-  asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-      : "r"(addr));
-  return v;
-}
 __device__ __forceinline__ float logaddexp_f(float a, float b) {
   const float mx = fmaxf(a, b), mn = fminf(a, b);
   if (mx == -INFINITY) return -INFINITY;
   return mx + log1pf(expf(mn - mx));
 }
+__host__ __device__ __forceinline__ int row_lo(int r, int S) { return (r * BM) / S; }
 }  // namespace
 
 // One request's head in one thread (all bins in registers, KB >= k compile-time bound).
@@ -243,7 +165,7 @@ __device__ __forceinline__ void head_one(int j, const float (&z)[KB] /* incl. b2
 }
 
 template <int KB>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(THREADS, 1)
 trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_x,
                            const __grid_constant__ CUtensorMap tmap_w, int n, int H, int kblocks,
                            int splits, const float *__restrict__ b1, const float *__restrict__ w2,
@@ -253,153 +175,214 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_x,
                            const float *__restrict__ prior_override, int max_slots,
                            float *__restrict__ lq_state, SlotMeta *__restrict__ meta,
                            float *__restrict__ post, float *__restrict__ Lout,
-                           uint32_t *__restrict__ err) {
-  extern __shared__ __align__(1024) uint8_t smem[];
+                           uint32_t *__restrict__ err, uint64_t *__restrict__ trace) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the SW128 operand tiles; offsetting the __shared__ array (not
+  // casting through an integer) keeps every epilogue access an LDS/STS, not a generic LD/ST
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + BAR_OFF);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + BAR_OFF + 8 * (2 * STAGES + 1));
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + BAR_OFF + 8 * (2 * STAGES + 2));
   uint32_t *flag = tmem_slot + 1;
-  float *w2s = reinterpret_cast<float *>(smem + W2_OFF);   // [k][BN]
+  float *w2s = reinterpret_cast<float *>(smem + W2_OFF);   // [KB][BN], rows >= k zero
   float *b1s = w2s + W2_FLOATS;                            // [BN]
   float *tile = reinterpret_cast<float *>(smem);           // [BM][TILE_LD] after the mainloop
   const uint32_t sA0 = smem_u32(smem), sB0 = sA0 + STAGES * A_BYTES;
-  const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * STAGES, done = full0 + 16 * STAGES;
+  const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * STAGES;
+  const uint32_t done = full0 + 16 * STAGES, land = done + 8;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  // diagnostics (trail_trace_*): per-CTA phase timestamps, globaltimer ns
+  uint64_t *tr = trace ? trace + 16 * (int64_t)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) : nullptr;
+  if (tr && tid == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tr[0] = gtimer();
+    tr[15] = smid;
+  }
   const int m0 = blockIdx.x * BM, nt = blockIdx.y, n0 = nt * BN, NT = gridDim.y;
-  const int s = blockIdx.z;
-  const uint32_t crank = splits > 1 ? cluster_rank() : 0u;
+  const int S = splits;
+  const int crank = S > 1 ? (int)cluster_rank() : 0;
   const int k = cst->k;
-  const int kb0 = (int)((int64_t)s * kblocks / splits);
-  const int kb1 = (int)((int64_t)(s + 1) * kblocks / splits);
+  const int kb0 = (int)((int64_t)crank * kblocks / S);
+  const int kb1 = (int)((int64_t)(crank + 1) * kblocks / S);
   const int nkb = kb1 - kb0;
+  const int r0 = row_lo(crank, S), rows = row_lo(crank + 1, S) - r0;
+  const int slot_rows = (BM + S - 1) / S;                  // landing slot size (rows)
 
-  // constant operands of the epilogue (weights: not produced by an earlier kernel)
-  for (int b = 0; b < k; ++b) w2s[b * BN + tid] = __ldg(w2 + (int64_t)b * H + n0 + tid);
-  b1s[tid] = __ldg(b1 + n0 + tid);
   if (tid == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(full0 + 8 * i, 1);
       mbar_init(empty0 + 8 * i, 1);
     }
     mbar_init(done, 1);
+    mbar_init(land, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_w)) : "memory");
   }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"((uint32_t)BN)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if (warp == 0) tmem_alloc(smem_u32(tmem_slot), (uint32_t)BN);
+  tc_fence_before();
   __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // the landing barrier's single arrival, carrying the bytes the S-1 peers will push
+  if (tid == 0 && S > 1) mbar_expect_tx(land, (uint32_t)((S - 1) * rows * ROW_BYTES));
   griddep_wait();     // X from the pool kernel, slot state from the previous step
   griddep_launch();
+  if (tr && tid == 0) tr[1] = gtimer();
 
-  if (warp == 0 && lane == 0) {
-    for (int i = 0; i < nkb; ++i) {
-      const int st = i % STAGES;
-      const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-      mbar_wait(empty0 + 8 * st, ph ^ 1u);
-      mbar_expect_tx(full0 + 8 * st, STAGE_BYTES);
-      const int kc = (kb0 + i) * BK;
-      tma_load_2d(sA0 + st * A_BYTES, &tmap_x, full0 + 8 * st, kc, m0);
-      tma_load_2d(sB0 + st * B_BYTES, &tmap_w, full0 + 8 * st, kc, n0);
+  // roles: lane 0 of warp 0 = TMA producer, lane 0 of warp 1 = MMA issuer; the other lanes
+  // of those warps park at __syncwarp; warps 2-7 stage the epilogue weights meanwhile
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int st = i % STAGES;
+        const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+        mbar_wait(empty0 + 8 * st, ph ^ 1u);
+        mbar_expect_tx(full0 + 8 * st, STAGE_BYTES);
+        const int kc = (kb0 + i) * BK;
+        tma_load_2d(sA0 + st * A_BYTES, &tmap_x, full0 + 8 * st, kc, m0);
+        tma_load_2d(sB0 + st * B_BYTES, &tmap_w, full0 + 8 * st, kc, n0);
+      }
     }
-  } else if (warp == 1 && lane == 0) {
-    constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
-    for (int i = 0; i < nkb; ++i) {
-      const int st = i % STAGES;
-      const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-      mbar_wait(full0 + 8 * st, ph);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t da = sw128_kmajor_desc(sA0 + st * A_BYTES);
-      const uint64_t db = sw128_kmajor_desc(sB0 + st * B_BYTES);
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+      for (int i = 0; i < nkb; ++i) {
+        const int st = i % STAGES;
+        const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+        mbar_wait(full0 + 8 * st, ph);
+        if (tr && i == 0) tr[2] = gtimer();
+        tc_fence_after();
+        const uint64_t da = sw128_kmajor_desc(sA0 + st * A_BYTES);
+        const uint64_t db = sw128_kmajor_desc(sB0 + st * B_BYTES);
 #pragma unroll
-      for (int kk = 0; kk < BK / 16; ++kk)
-        umma_bf16(tmem, da + 2 * kk, db + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : 0u);
-      umma_commit(empty0 + 8 * st);
+        for (int kk = 0; kk < BK / 16; ++kk)
+          umma_bf16(tmem, da + 2 * kk, db + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(empty0 + 8 * st);
+      }
+      umma_commit(done);
     }
-    umma_commit(done);
+    __syncwarp();
+  } else {
+    // W2[:, n0:n0+BN] (zero rows for b >= k) and b1[n0:n0+BN]: weights, not produced by an
+    // earlier kernel; 192 threads, float4 loads all in flight
+    const int t = tid - 64;
+    constexpr int NV = KB * (BN / 4);
+#pragma unroll
+    for (int v0 = 0; v0 < NV; v0 += THREADS - 64) {
+      const int v = v0 + t;
+      if (v < NV) {
+        const int b = v / (BN / 4), c = (v % (BN / 4)) * 4;
+        float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (b < k) w = __ldg(reinterpret_cast<const float4 *>(w2 + (int64_t)b * H + n0 + c));
+        *reinterpret_cast<float4 *>(w2s + b * BN + c) = w;
+      }
+    }
+    if (t < BN / 4)
+      *reinterpret_cast<float4 *>(b1s + 4 * t) =
+          __ldg(reinterpret_cast<const float4 *>(b1 + n0 + 4 * t));
   }
 
   // ---- 1. partial tile: TMEM -> own shared memory (pipeline buffers are idle now)
   mbar_wait(done, 0);
   __syncwarp();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll 1
-  for (int c = 0; c < BN; c += 32) {
-    uint32_t r[32];
-    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, r);
-    float4 *dst = reinterpret_cast<float4 *>(tile + (warp * 32 + lane) * TILE_LD + c);
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                           __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  if (splits > 1) cluster_sync(); else __syncthreads();
-
-  // ---- 2. reduce my row group over the cluster, bias + ReLU, layer-2 partial logits
-  const int rows = BM / splits;                 // rows reduced by this CTA (16 for S = 8)
-  const int r0 = (int)crank * rows;
-  const int tpr = 128 / rows;                   // threads per row (8 for S = 8)
-  const int cols = BN / tpr;                    // columns per thread (16 for S = 8)
-  const int rr = tid / tpr, cg = tid % tpr;
-  const int grow = m0 + r0 + rr;                // request index
-  float zp[KB];
-#pragma unroll
-  for (int b = 0; b < KB; ++b) zp[b] = 0.f;
+  if (tr && tid == 0) tr[3] = gtimer();
+  tc_fence_after();
   {
-    const uint32_t base = smem_u32(tile + (r0 + rr) * TILE_LD + cg * cols);
-    uint32_t rbase[MAXS];
+    const int g = warp & 3, half = warp >> 2;
+    const int row = 32 * g + lane;
 #pragma unroll
-    for (int p = 0; p < MAXS; ++p) rbase[p] = (splits > 1 && p < splits) ? mapa(base, p) : base;
-    for (int c4 = 0; c4 < cols / 4; ++c4) {
-      float4 v[MAXS];
+    for (int cc = 0; cc < 64; cc += 32) {
+      const int c = 64 * half + cc;
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)c, r);
+      float4 *dst = reinterpret_cast<float4 *>(tile + row * TILE_LD + c);
 #pragma unroll
-      for (int p = 0; p < MAXS; ++p)             // all S loads in flight, then a fixed-order sum
-        if (p < splits) v[p] = ld_cluster_f4(rbase[p] + 16 * c4);
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < 8; ++q)
+        dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                             __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+    }
+  }
+  tc_fence_before();
+  fence_proxy_async_smem();          // the tile is read by the bulk-copy (async) proxy
+  if (tr && tid == 0) tr[4] = gtimer();
+  if (S > 1) cluster_sync(); else __syncthreads();
+  if (tr && tid == 0) tr[5] = gtimer();
+
+  // ---- 2. push row group p of my partial tile to CTA p (one bulk copy per peer)
+  const uint32_t land_base = smem_u32(smem + LAND_OFF);
+  if (S > 1) {
+    if (tid == 0) {
+      for (int q = 1; q < S; ++q) {
+        const int p = (crank + q) % S;
+        const int pr0 = row_lo(p, S), prows = row_lo(p + 1, S) - pr0;
+        const uint32_t src = smem_u32(tile + pr0 * TILE_LD);
+        const uint32_t dst = mapa(land_base + (uint32_t)(crank * slot_rows * ROW_BYTES), (uint32_t)p);
+        bulk_s2cluster(dst, src, (uint32_t)(prows * ROW_BYTES), mapa(land, (uint32_t)p));
+      }
+    }
+    mbar_wait(land, 0);
+    cluster_arrive();                // "my slices have landed" (waited on before exit)
+  }
+  if (tr && tid == 0) tr[6] = gtimer();
+
+  // ---- 3. fixed-order sum over the S partials, b1, ReLU, layer-2 partial logits
+  {
+    // 32 rows x 8 column lanes per pass; lane cg owns columns 4cg + 32c4 (c4 = 0..3), so the
+    // 8 lanes of a row read 128 contiguous bytes of W2 / the tile: no bank conflicts
+    const int rg = tid >> 3, cg = tid & 7;
+    const int col0 = cg * 4;
+    const float *land_f = reinterpret_cast<const float *>(smem + LAND_OFF);
+    for (int rb = 0; rb < rows; rb += THREADS / 8) {
+      const int row = rb + rg;
+      const bool valid = row < rows;
+      const int rr = valid ? row : 0;
+      float zp[KB];
 #pragma unroll
-      for (int p = 0; p < MAXS; ++p)
-        if (p < splits) { acc.x += v[p].x; acc.y += v[p].y; acc.z += v[p].z; acc.w += v[p].w; }
-      const int col = cg * cols + 4 * c4;
-      const float h0 = fmaxf(acc.x + b1s[col], 0.f), h1 = fmaxf(acc.y + b1s[col + 1], 0.f);
-      const float h2 = fmaxf(acc.z + b1s[col + 2], 0.f), h3 = fmaxf(acc.w + b1s[col + 3], 0.f);
+      for (int b = 0; b < KB; ++b) zp[b] = 0.f;
 #pragma unroll
-      for (int b = 0; b < KB; ++b) {
-        if (b < k) {
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const int col = col0 + 32 * c4;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+        for (int p = 0; p < S; ++p) {
+          const float *src = p == crank ? tile + (r0 + rr) * TILE_LD + col
+                                        : land_f + (p * slot_rows + rr) * TILE_LD + col;
+          const float4 v = *reinterpret_cast<const float4 *>(src);
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        const float4 bb = *reinterpret_cast<const float4 *>(b1s + col);
+        const float h0 = fmaxf(acc.x + bb.x, 0.f), h1 = fmaxf(acc.y + bb.y, 0.f);
+        const float h2 = fmaxf(acc.z + bb.z, 0.f), h3 = fmaxf(acc.w + bb.w, 0.f);
+#pragma unroll
+        for (int b = 0; b < KB; ++b) {
           const float4 w = *reinterpret_cast<const float4 *>(w2s + b * BN + col);
           zp[b] = fmaf(w.x, h0, fmaf(w.y, h1, fmaf(w.z, h2, fmaf(w.w, h3, zp[b]))));
         }
       }
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+#pragma unroll
+        for (int b = 0; b < KB; ++b) zp[b] += __shfl_xor_sync(0xffffffffu, zp[b], o);
+      }
+      const int grow = m0 + r0 + row;
+      if (valid && cg == 0 && grow < n) {
+        float *zo = zpart + ((int64_t)grow * NT + nt) * k;
+#pragma unroll
+        for (int b = 0; b < KB; ++b)
+          if (b < k) zo[b] = zp[b];
+      }
     }
   }
-  // reduce over the tpr threads of a row (consecutive lanes)
-  for (int o = 1; o < tpr; o <<= 1) {
-#pragma unroll
-    for (int b = 0; b < KB; ++b)
-      if (b < k) zp[b] += __shfl_xor_sync(0xffffffffu, zp[b], o);
-  }
-  if (cg == 0 && grow < n) {
-    float *zo = zpart + ((int64_t)grow * NT + nt) * k;
-#pragma unroll
-    for (int b = 0; b < KB; ++b)
-      if (b < k) zo[b] = zp[b];
-  }
-  // peers must finish reading my tile before this CTA exits
-  if (splits > 1) cluster_sync();
+  if (tr && tid == 0) tr[7] = gtimer();
 
-  // ---- 3. last column tile of this row group runs the head
+  // ---- 4. last column tile of this row group runs the head
   __threadfence();
   __syncthreads();
   if (tid == 0) {
-    uint32_t *cnt = arrive_cnt + (int64_t)blockIdx.x * splits + crank;
+    uint32_t *cnt = arrive_cnt + (int64_t)blockIdx.x * MAXS + crank;
     const uint32_t old = atomicAdd(cnt, 1u);
     const bool last = old == (uint32_t)(NT - 1);
     if (last) *cnt = 0u;                        // re-arm for the next launch
@@ -428,11 +411,10 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_x,
       }
     }
   }
+  if (S > 1) cluster_wait();         // every CTA's incoming slices landed: my copies are done
   __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"((uint32_t)BN)
-                 : "memory");
+  if (tr && tid == 0) { tr[8] = gtimer(); tr[14] = *flag; }
+  if (warp == 0) tmem_dealloc(tmem, (uint32_t)BN);
 }
 
 // ------------------------------------------------------------------ host
@@ -445,22 +427,64 @@ static cudaError_t fused_attr() {
                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }
 
+template <int KB>
+static cudaError_t fused_occupancy(Ctx &c) {
+  for (int s = 1; s <= MAXS; ++s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1, 1, s);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SMEM_TOTAL;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, trail_fused_predict_kernel<KB>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      nc = 0;
+    }
+    c.fused_max_clusters[s] = nc;
+  }
+  return cudaSuccess;
+}
+
+static int fused_kb(int k) { return k <= 10 ? 10 : k <= 16 ? 16 : k <= 20 ? 20 : 32; }
+
 cudaError_t fused_prepare(Ctx &c) {
   if (c.dtype != TRAIL_BF16) return cudaSuccess;
   cudaError_t e = fused_attr<10>();
   if (e == cudaSuccess) e = fused_attr<16>();
   if (e == cudaSuccess) e = fused_attr<20>();
   if (e == cudaSuccess) e = fused_attr<32>();
-  return e;
+  if (e != cudaSuccess) return e;
+  switch (fused_kb(c.k)) {
+    case 10: return fused_occupancy<10>(c);
+    case 16: return fused_occupancy<16>(c);
+    case 20: return fused_occupancy<20>(c);
+    default: return fused_occupancy<32>(c);
+  }
 }
 
+// Split-K factor: the largest SM coverage (tiles x S) for which every cluster of S CTAs is
+// resident at once (one wave; the cluster barrier requires co-residency anyway), S <= 16
+// and S <= the number of 64-wide K blocks.  Ties go to the smaller S (less exchange).
 int fused_splits(const Ctx &c, int n) {
   const int tiles = ((n + BM - 1) / BM) * (c.H / BN);
   const int kblocks = c.d / BK;
-  int s = std::max(1, c.num_sms / std::max(1, tiles));
-  int p = 1;
-  while (p * 2 <= std::min(std::min(s, MAXS), kblocks)) p *= 2;   // power of two <= 16
-  return p;
+  if (const char *e = getenv("TRAIL_FUSED_SPLITS")) {
+    const int v = atoi(e);
+    if (v >= 1 && v <= MAXS) return std::min(v, kblocks);
+  }
+  int best = 1, best_cov = 0;
+  for (int s = 1; s <= std::min(MAXS, kblocks); ++s) {
+    const int maxc = c.fused_max_clusters[s];
+    if (maxc <= 0 || tiles > maxc) continue;
+    if (tiles * s > best_cov) { best_cov = tiles * s; best = s; }
+  }
+  return best;
 }
 
 cudaError_t launch_fused_predict(const Ctx &c, int n, int splits, const uint32_t *ids,
@@ -469,7 +493,7 @@ cudaError_t launch_fused_predict(const Ctx &c, int n, int splits, const uint32_t
   if (!c.have_tmaps) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((n + BM - 1) / BM, c.H / BN, splits);
-  cfg.blockDim = dim3(128);
+  cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = SMEM_TOTAL;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
@@ -486,16 +510,21 @@ cudaError_t launch_fused_predict(const Ctx &c, int n, int splits, const uint32_t
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
+  uint64_t *trace =
+      (c.trace && (int)(cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z) <= c.trace_cap) ? c.trace
+                                                                                       : nullptr;
 #define TRAIL_FUSED(KB)                                                                          \
   return cudaLaunchKernelEx(&cfg, trail_fused_predict_kernel<KB>, c.tmap_x, c.tmap_w128, n, c.H,  \
                             c.d / BK, splits, (const float *)c.b1, (const float *)c.w2,           \
                             (const float *)c.b2, (const HeadConsts *)c.consts, c.zpart,           \
                             c.arrive_cnt, ids, is_prefill, prior_override, c.cfg.max_slots, c.lq, \
-                            c.meta, post, L, c.dev_err)
-  if (c.k <= 10) TRAIL_FUSED(10);
-  if (c.k <= 16) TRAIL_FUSED(16);
-  if (c.k <= 20) TRAIL_FUSED(20);
-  TRAIL_FUSED(32);
+                            c.meta, post, L, c.dev_err, trace)
+  switch (fused_kb(c.k)) {
+    case 10: TRAIL_FUSED(10);
+    case 16: TRAIL_FUSED(16);
+    case 20: TRAIL_FUSED(20);
+    default: TRAIL_FUSED(32);
+  }
 #undef TRAIL_FUSED
 }
 

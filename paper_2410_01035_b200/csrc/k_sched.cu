@@ -272,6 +272,7 @@ cudaError_t select_prepare(Ctx &c) {
   (void)c;
   cudaError_t e = select_fast_prepare();
   if (e == cudaSuccess) e = select_radix_prepare();
+  if (e == cudaSuccess) e = select_rank_prepare();
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(trail_select_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               kSmemCapRecords * 12);
@@ -280,7 +281,10 @@ cudaError_t select_prepare(Ctx &c) {
 cudaError_t launch_select(const Ctx &c, const Record *rec, int n, int64_t budget, int max_run,
                           uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
                           cudaStream_t s) {
-  if (!use_bitonic_select() && n <= select_radix_capacity())
+  if (select_impl() == 0 && n <= select_rank_capacity())
+    return launch_select_rank(c, rec, nullptr, nullptr, nullptr, nullptr, nullptr, n, budget,
+                              max_run, run, pre, adm, counts, s);
+  if (select_impl() != 2 && n <= select_radix_capacity())
     return launch_select_radix(c, rec, nullptr, nullptr, nullptr, nullptr, nullptr, n, budget,
                                max_run, run, pre, adm, counts, s);
   if (n <= select_fast_capacity())

@@ -132,7 +132,8 @@ trail_status set_device(const Ctx &c) {
 
 void free_ctx(Ctx &c) {
   void *ptrs[] = {c.w1, c.b1, c.w2, c.b2, c.consts, c.lq, c.meta, c.dev_err, c.xs,
-                  c.partial, c.rec_local, c.rec_all, c.sel_scratch, c.zpart, c.arrive_cnt};
+                  c.partial, c.rec_local, c.rec_all, c.sel_scratch, c.zpart, c.arrive_cnt, c.trace,
+                  c.rank_sorted, c.rank_cnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c.prof_ev) {
@@ -283,6 +284,9 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
   const int max_sched = std::max(1, g.max_sched);
   ALLOC(c.rec_local, (size_t)max_sched * sizeof(Record));
   ALLOC(c.rec_all, (size_t)max_sched * c.world * sizeof(Record));
+  ALLOC(c.rank_sorted, (size_t)max_sched * c.world * sizeof(Record));
+  ALLOC(c.rank_cnt, 16 * sizeof(uint32_t));
+  if (cudaMemset(c.rank_cnt, 0, 16 * sizeof(uint32_t)) != cudaSuccess) return fail(TRAIL_ERR_CUDA);
   c.sel_scratch_bytes = select_scratch_bytes(max_sched * c.world);
   if (c.sel_scratch_bytes) ALLOC(c.sel_scratch, c.sel_scratch_bytes);
   const size_t m_tiles = ((size_t)g.max_requests + 127) / 128;
@@ -317,6 +321,35 @@ trail_status trail_destroy(trail_handle h) {
   cudaDeviceSynchronize();
   free_ctx(h->c);
   delete h;
+  return TRAIL_OK;
+}
+
+trail_status trail_trace_enable(trail_handle h, int32_t max_ctas) {
+  if (!h || max_ctas < 0) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  if (c.trace) {
+    TRAIL_CUDA(cudaDeviceSynchronize());
+    cudaFree(c.trace);
+    c.trace = nullptr;
+    c.trace_cap = 0;
+  }
+  if (max_ctas == 0) return TRAIL_OK;
+  if (cudaMalloc((void **)&c.trace, (size_t)max_ctas * 16 * sizeof(uint64_t)) != cudaSuccess)
+    return TRAIL_ERR_NOMEM;
+  TRAIL_CUDA(cudaMemset(c.trace, 0, (size_t)max_ctas * 16 * sizeof(uint64_t)));
+  c.trace_cap = max_ctas;
+  return TRAIL_OK;
+}
+
+trail_status trail_trace_read(trail_handle h, uint64_t *host_out, int32_t max_ctas) {
+  if (!h || !host_out || max_ctas < 0) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (!c.trace) return TRAIL_ERR_STATE;
+  if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  TRAIL_CUDA(cudaDeviceSynchronize());
+  const size_t nb = (size_t)std::min(max_ctas, c.trace_cap) * 16 * sizeof(uint64_t);
+  TRAIL_CUDA(cudaMemcpy(host_out, c.trace, nb, cudaMemcpyDeviceToHost));
   return TRAIL_OK;
 }
 
@@ -429,17 +462,12 @@ trail_status trail_schedule_step(trail_handle h, const uint32_t *request_ids,
   if (c.world > 1 && !c.nccl_comm) return TRAIL_ERR_STATE;
   if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
   cudaStream_t s = (cudaStream_t)stream;
-  if (!c.nccl_comm && n <= select_radix_capacity()) {
+  if (!c.nccl_comm && n <= select_local_capacity()) {
     // local selection: the record build is fused into the selection kernel
     ProfScope p(c, TRAIL_K_SELECT, s);
-    if (use_bitonic_select())
-      TRAIL_CUDA(launch_select_fast(c, nullptr, c.rec_local, request_ids, arrival_seq, kv_blocks,
-                                    is_running, n, kv_budget, max_run, run_ids, preempt_ids,
-                                    admit_ids, counts, s));
-    else
-      TRAIL_CUDA(launch_select_radix(c, nullptr, c.rec_local, request_ids, arrival_seq,
-                                     kv_blocks, is_running, n, kv_budget, max_run, run_ids,
-                                     preempt_ids, admit_ids, counts, s));
+    TRAIL_CUDA(launch_select_local(c, request_ids, arrival_seq, kv_blocks, is_running, n,
+                                   kv_budget, max_run, run_ids, preempt_ids, admit_ids, counts,
+                                   s));
     return TRAIL_OK;
   }
   const int npad = c.nccl_comm ? std::max(1, c.cfg.max_sched) : n;
@@ -603,12 +631,38 @@ bool pdl_enabled() {
   }
   return v == 1;
 }
-bool use_bitonic_select() {
+// Selection kernel: default = multi-CTA rank counting (k_rank.cu) up to its capacity;
+// TRAIL_SELECT=radix / bitonic forces the single-CTA radix or bitonic kernels (comparisons).
+int select_impl() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("TRAIL_SELECT");
-    v = (e && e[0] == 'b') ? 1 : 0;
+    v = (e && e[0] == 'b') ? 2 : (e && e[0] == 'r') ? 1 : 0;
   }
-  return v == 1;
+  return v;
+}
+bool use_bitonic_select() { return select_impl() == 2; }
+int select_local_capacity() {
+  switch (select_impl()) {
+    case 0: return select_rank_capacity();
+    case 1: return select_radix_capacity();
+    default: return select_fast_capacity();
+  }
+}
+cudaError_t launch_select_local(const Ctx &c, const uint32_t *ids, const uint32_t *arrival,
+                                const int32_t *kv, const uint8_t *running, int n, int64_t budget,
+                                int max_run, uint32_t *run, uint32_t *pre, uint32_t *adm,
+                                int32_t *counts, cudaStream_t s) {
+  switch (select_impl()) {
+    case 0:
+      return launch_select_rank(c, nullptr, c.rec_local, ids, arrival, kv, running, n, budget,
+                                max_run, run, pre, adm, counts, s);
+    case 1:
+      return launch_select_radix(c, nullptr, c.rec_local, ids, arrival, kv, running, n, budget,
+                                 max_run, run, pre, adm, counts, s);
+    default:
+      return launch_select_fast(c, nullptr, c.rec_local, ids, arrival, kv, running, n, budget,
+                                max_run, run, pre, adm, counts, s);
+  }
 }
 }  // namespace trail

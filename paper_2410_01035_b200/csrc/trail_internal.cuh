@@ -63,6 +63,11 @@ struct Ctx {
   size_t partial_elems = 0;
   float *zpart = nullptr;      // [max_requests][H/128][k] fused kernel: layer-2 partial logits
   uint32_t *arrive_cnt = nullptr;  // [m_tiles][16] fused kernel: column-tile arrival counters
+  uint64_t *trace = nullptr;   // diagnostics: per-CTA phase timestamps (trail_trace_enable)
+  int trace_cap = 0;           // CTAs the trace buffer holds (16 u64 each)
+  int fused_max_clusters[17] = {};
+  Record *rank_sorted = nullptr;    // [max_sched * world] rank-select scatter target
+  uint32_t *rank_cnt = nullptr;     // rank-select CTA completion counter  // fused kernel: resident clusters of size s (occupancy)
   Record *rec_local = nullptr; // [max_sched]
   Record *rec_all = nullptr;   // [max_sched * world]
   void *sel_scratch = nullptr; // global scratch for large selections
@@ -122,6 +127,19 @@ cudaError_t launch_select_radix(const Ctx &c, const Record *rec_in, Record *rec_
                                 uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
                                 cudaStream_t s);
 bool use_bitonic_select();
+int select_impl();
+int select_local_capacity();
+cudaError_t launch_select_local(const Ctx &c, const uint32_t *ids, const uint32_t *arrival,
+                                const int32_t *kv, const uint8_t *running, int n, int64_t budget,
+                                int max_run, uint32_t *run, uint32_t *pre, uint32_t *adm,
+                                int32_t *counts, cudaStream_t s);
+cudaError_t select_rank_prepare();
+int select_rank_capacity();
+cudaError_t launch_select_rank(const Ctx &c, const Record *rec_in, Record *rec_out,
+                               const uint32_t *ids, const uint32_t *arrival, const int32_t *kv,
+                               const uint8_t *running, int n, int64_t budget, int max_run,
+                               uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
+                               cudaStream_t s);
 cudaError_t select_fast_prepare();
 int select_fast_capacity();
 // rec_in != nullptr: select over given records; else build local records (fused pack)

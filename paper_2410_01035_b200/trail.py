@@ -79,6 +79,8 @@ _SIGS = {
     "trail_profile_read": ([_P, _I32, ctypes.POINTER(ctypes.c_double),
                             ctypes.POINTER(ctypes.c_int64), _I32], _I32),
     "trail_set_l1_mode": ([_P, _I32], _I32),
+    "trail_trace_enable": ([_P, _I32], _I32),
+    "trail_trace_read": ([_P, _P, _I32], _I32),
     "trail_plan_l1": ([_P, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)], _I32),
 }
 
@@ -218,6 +220,16 @@ def trail_profile_read(h, kernel: str, reset: bool = False):
     _check("trail_profile_read", _lib().trail_profile_read(h, TRAIL_K[kernel], ctypes.byref(ms),
                                                            ctypes.byref(cnt), int(reset)))
     return float(ms.value), int(cnt.value)
+
+
+def trail_trace_enable(h, max_ctas: int) -> None:
+    _check("trail_trace_enable", _lib().trail_trace_enable(h, int(max_ctas)))
+
+
+def trail_trace_read(h, max_ctas: int) -> np.ndarray:
+    out = np.zeros((int(max_ctas), 16), dtype=np.uint64)
+    _check("trail_trace_read", _lib().trail_trace_read(h, out.ctypes.data, int(max_ctas)))
+    return out
 
 
 def trail_set_l1_mode(h, mode: int) -> None:
