@@ -84,7 +84,7 @@ typedef struct {
                               c >= 0; INFINITY = unlimited (reading D-14)                  */
   /* Capacities (fixed for the handle's lifetime). */
   int32_t max_slots;       /* request ids are slot indices in [0, max_slots)              */
-  int32_t max_requests;    /* max n per trail_predict_step                                */
+  int32_t max_requests;    /* max n per trail_predict_step, <= 262144                      */
   int32_t max_sched;       /* max records per trail_schedule_step on THIS rank            */
   int32_t world_size;      /* ranks sharing one selection (1 = single GPU)                */
   uint32_t id_base;        /* added to slot ids in the returned lists (e.g. rank*max_slots) */

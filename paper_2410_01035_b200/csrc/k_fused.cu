@@ -166,8 +166,14 @@ __device__ __forceinline__ void head_one(int j, const float (&z)[KB] /* incl. b2
 
 template <int KB>
 __global__ void __launch_bounds__(THREADS, 1)
-trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_x,
-                           const __grid_constant__ CUtensorMap tmap_w, int n, int H, int kblocks,
+trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
+                           const __grid_constant__ CUtensorMap tmap_emb4,
+                           const __grid_constant__ CUtensorMap tmap_emb32,
+                           const __grid_constant__ CUtensorMap tmap_xs,
+                           const __grid_constant__ CUtensorMap tmap_xs4,
+                           const __grid_constant__ CUtensorMap tmap_xs32,
+                           const __grid_constant__ CUtensorMap tmap_w,
+                           const int32_t *__restrict__ off, int n, int H, int kblocks,
                            int splits, const float *__restrict__ b1, const float *__restrict__ w2,
                            const float *__restrict__ b2, const HeadConsts *__restrict__ cst,
                            float *__restrict__ zpart, uint32_t *__restrict__ arrive_cnt,
@@ -217,7 +223,9 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_x,
     mbar_init(done, 1);
     mbar_init(land, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_emb)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_emb32)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_xs32)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_w)) : "memory");
   }
   if (warp == 0) tmem_alloc(smem_u32(tmem_slot), (uint32_t)BN);
@@ -227,25 +235,94 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_x,
   const uint32_t tmem = *tmem_slot;
   // the landing barrier's single arrival, carrying the bytes the S-1 peers will push
   if (tid == 0 && S > 1) mbar_expect_tx(land, (uint32_t)((S - 1) * rows * ROW_BYTES));
-  griddep_wait();     // X from the pool kernel, slot state from the previous step
   griddep_launch();
   if (tr && tid == 0) tr[1] = gtimer();
 
   // roles: lane 0 of warp 0 = TMA producer, lane 0 of warp 1 = MMA issuer; the other lanes
-  // of those warps park at __syncwarp; warps 2-7 stage the epilogue weights meanwhile
+  // of those warps park at __syncwarp; warps 2-7 stage the epilogue weights meanwhile.
+  // PDL: only the producer's X loads depend on the previous kernel (the pool kernel writes
+  // X), so the W1 tiles of the first STAGES stages are requested before griddep_wait and
+  // the prologue + first weight fetches overlap the previous kernel's tail.  Every other
+  // thread waits before the epilogue, which reads the slot state.
   if (warp == 0) {
-    if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
-        const int st = i % STAGES;
-        const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-        mbar_wait(empty0 + 8 * st, ph ^ 1u);
-        mbar_expect_tx(full0 + 8 * st, STAGE_BYTES);
-        const int kc = (kb0 + i) * BK;
-        tma_load_2d(sA0 + st * A_BYTES, &tmap_x, full0 + 8 * st, kc, m0);
-        tma_load_2d(sB0 + st * B_BYTES, &tmap_w, full0 + 8 * st, kc, n0);
+    // A operand = the n x d embedding matrix X, gathered row by row (row a1): request j's row
+    // is emb row off[j] when it has exactly one row (decode: bit-exact), else the
+    // pooled prompt mean the pool kernel wrote to xs row j (prefill).  Lane l owns rows
+    // 4l..4l+3 of the tile: one TMA tile::gather4 per k-block when all four come from emb,
+    // else four single-row loads.  Only xs rows depend on the previous kernel (PDL): decode
+    // tiles never wait for the pool kernel.
+    int src[4];
+    unsigned emask = 0u;                       // bit q: row 4*lane+q comes from emb
+    bool any_xs = false;
+    {
+      const int j4 = m0 + 4 * lane;
+      int o[5];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) o[q] = (j4 + q <= n) ? __ldg(off + j4 + q) : 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = j4 + q;
+        const bool single = j < n && o[q + 1] - o[q] == 1;
+        src[q] = single ? o[q] : j;            // emb row, or xs row (padding rows: xs, unused)
+        emask |= single ? 1u << q : 0u;
+        any_xs |= !single && j < n;
       }
     }
+    // load plan of my 4-row group: runs of consecutive source rows become one TMA box
+    // (32 rows per 8-lane block, else 4 rows), scattered single rows a gather4, mixed
+    // groups four 1-row loads
+    const bool g_emb = emask == 0xFu, g_xs = emask == 0u;
+    const bool g_contig = src[1] == src[0] + 1 && src[2] == src[0] + 2 && src[3] == src[0] + 3;
+    const int prev_src0 = __shfl_up_sync(0xffffffffu, src[0], 1);
+    const bool link = (lane & 7) == 0 || prev_src0 + 4 == src[0];
+    const unsigned blk = 0xFFu << (lane & 24);
+    const bool b_emb = (__ballot_sync(0xffffffffu, g_emb && g_contig && link) & blk) == blk;
+    const bool b_xs = (__ballot_sync(0xffffffffu, g_xs && g_contig && link) & blk) == blk;
+    // mode: 0 none (covered by the block op), 1 block emb32, 2 block xs32, 3 emb4, 4 xs4,
+    //       5 gather4 (emb), 6 four single rows
+    int mode;
+    if (b_emb || b_xs) mode = (lane & 7) == 0 ? (b_emb ? 1 : 2) : 0;
+    else if (g_contig && g_emb) mode = 3;
+    else if (g_contig && g_xs) mode = 4;
+    else if (g_emb) mode = 5;
+    else mode = 6;
+    const bool tile_xs = __any_sync(0xffffffffu, any_xs);
+    const int pre = nkb < STAGES ? nkb : STAGES;
+    if (lane == 0)
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx(full0 + 8 * i, STAGE_BYTES);
+        tma_load_2d(sB0 + i * B_BYTES, &tmap_w, full0 + 8 * i, (kb0 + i) * BK, n0);
+      }
+    if (tile_xs) griddep_wait();
     __syncwarp();
+    for (int i = 0; i < nkb; ++i) {
+      const int st = i % STAGES;
+      const int kc = (kb0 + i) * BK;
+      if (i >= STAGES) {
+        if (lane == 0) {
+          const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+          mbar_wait(empty0 + 8 * st, ph ^ 1u);
+          mbar_expect_tx(full0 + 8 * st, STAGE_BYTES);
+          tma_load_2d(sB0 + st * B_BYTES, &tmap_w, full0 + 8 * st, kc, n0);
+        }
+        __syncwarp();
+      }
+      const uint32_t dst = sA0 + st * A_BYTES + (uint32_t)(lane * 4 * 128);
+      const uint32_t fb = full0 + 8 * st;
+      switch (mode) {
+        case 1: tma_load_2d(dst, &tmap_emb32, fb, kc, src[0]); break;
+        case 2: tma_load_2d(dst, &tmap_xs32, fb, kc, src[0]); break;
+        case 3: tma_load_2d(dst, &tmap_emb4, fb, kc, src[0]); break;
+        case 4: tma_load_2d(dst, &tmap_xs4, fb, kc, src[0]); break;
+        case 5: tma_gather4(dst, &tmap_emb, fb, kc, src[0], src[1], src[2], src[3]); break;
+        case 6:
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            tma_load_2d(dst + q * 128, ((emask >> q) & 1u) ? &tmap_emb : &tmap_xs, fb, kc, src[q]);
+          break;
+        default: break;
+      }
+    }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
@@ -285,6 +362,8 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_x,
           __ldg(reinterpret_cast<const float4 *>(b1 + n0 + 4 * t));
   }
 
+  // No griddep_wait for the epilogue: it reads only inputs, weights and slot state written by
+  // kernels that completed before the pool kernel passed its own griddep_wait (PDL chain).
   // ---- 1. partial tile: TMEM -> own shared memory (pipeline buffers are idle now)
   mbar_wait(done, 0);
   __syncwarp();
@@ -487,10 +566,20 @@ int fused_splits(const Ctx &c, int n) {
   return best;
 }
 
-cudaError_t launch_fused_predict(const Ctx &c, int n, int splits, const uint32_t *ids,
+cudaError_t launch_fused_predict(Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
+                                 int splits, const uint32_t *ids,
                                  const uint8_t *is_prefill, const float *prior_override,
                                  float *post, float *L, cudaStream_t s) {
   if (!c.have_tmaps) return cudaErrorInvalidValue;
+  if (emb != c.tmap_emb_ptr || ld != c.tmap_emb_ld) {   // row-gather map over the caller's rows
+    const uint64_t rows = 0x7FFFFFFF;     // rows are addressed through off[] only
+    if (!encode_rows_bf16(&c.tmap_emb, emb, (uint64_t)c.d, rows, (uint64_t)ld, BK, 1) ||
+        !encode_rows_bf16(&c.tmap_emb4, emb, (uint64_t)c.d, rows, (uint64_t)ld, BK, 4) ||
+        !encode_rows_bf16(&c.tmap_emb32, emb, (uint64_t)c.d, rows, (uint64_t)ld, BK, 32))
+      return cudaErrorInvalidValue;
+    c.tmap_emb_ptr = emb;
+    c.tmap_emb_ld = ld;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((n + BM - 1) / BM, c.H / BN, splits);
   cfg.blockDim = dim3(THREADS);
@@ -514,7 +603,9 @@ cudaError_t launch_fused_predict(const Ctx &c, int n, int splits, const uint32_t
       (c.trace && (int)(cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z) <= c.trace_cap) ? c.trace
                                                                                        : nullptr;
 #define TRAIL_FUSED(KB)                                                                          \
-  return cudaLaunchKernelEx(&cfg, trail_fused_predict_kernel<KB>, c.tmap_x, c.tmap_w128, n, c.H,  \
+  return cudaLaunchKernelEx(&cfg, trail_fused_predict_kernel<KB>, c.tmap_emb, c.tmap_emb4,       \
+                            c.tmap_emb32, c.tmap_xs1, c.tmap_xs4, c.tmap_xs32,                    \
+                            c.tmap_w128, off, n, c.H,                                             \
                             c.d / BK, splits, (const float *)c.b1, (const float *)c.w2,           \
                             (const float *)c.b2, (const HeadConsts *)c.consts, c.zpart,           \
                             c.arrive_cnt, ids, is_prefill, prior_override, c.cfg.max_slots, c.lq, \

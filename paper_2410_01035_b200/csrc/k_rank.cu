@@ -6,25 +6,35 @@
 // (stable) — run set = every forced record + the longest prefix of the rest within the KV
 // budget and the run cap (strict prefix, D-15; forced overflow -> D-16).
 //
-// Instead of one CTA sorting (a chain of ~60 block barriers), every CTA of a small grid
-// stages all n composite keys in shared memory and computes the exact rank of 64 records
-// by counting smaller keys (8 threads per record, keys broadcast from shared memory), then
-// scatters each record to its rank in a global array: all 148 SMs count in parallel, and
-// no barrier chain is on the critical path.  The last CTA to finish (release/acquire
-// counter) runs the linear part — one block scan over the sorted records gives the
-// cumulative KV, forced and running counts from which the cut and the run / preempt / admit
-// list positions follow directly.
+// Instead of one CTA sorting (a chain of ~60 block barriers), every CTA of a grid sized to
+// about one wave stages all n records (key, KV, flags; 16 B each) in shared memory, and for
+// each of its own records computes, in ONE pass over all keys (TPI threads per record),
+//   pos  = #records ordered before it       (its exact rank: run-list position),
+//   cum  = KV of the records before it       (+ its own KV: the cumulative KV at pos),
+//   rb   = #running records before it.
+// Because forced records sort first, cum includes the forced KV S_f, and the run set is
+//   in_run = forced  or  (not over-budget and cum_incl <= budget and pos < cap)
+// (the non-forced cumulative KV is monotone, so this is exactly the strict prefix), while
+// the list positions follow directly: run_ids[pos], admit_ids[pos - rb] (waiting records
+// before pos), and preempt_ids[rb - R(cut)] with R(cut) = running records in the run set —
+// the one global quantity, summed with atomics; the last CTA to finish writes the preempt
+// list from the (pos -> gid, rb) scratch array.  All SMs work in parallel; the only
+// serial part is one pass over the records past the cut.
 //
-// Local selection (rec_in == nullptr): every CTA builds the keys from the slot state
+// Local selection (rec_in == nullptr): every CTA builds the records from the slot state
 // (row a4: key = L_t, or E_pi[L] if never observed; forced = running and a >= floor(c r))
 // and the owner of a record writes it (16 B) to `rec_out` for trail_schedule_pack parity.
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "sm100_ptx.cuh"
 #include "trail_internal.cuh"
 
 namespace trail {
 
 namespace {
 constexpr int kT = 512;               // threads per CTA
-constexpr int kItems = kT / 8;        // records ranked per CTA
 constexpr int kRankCap = 8192;        // keys staged in shared memory (64 KB)
 
 struct RkShared {
@@ -126,194 +136,171 @@ __device__ __forceinline__ unsigned long long rk_key(const Record &r) {
 }
 }  // namespace
 
-template <int E>
+// Per-record state kept in shared memory by every CTA (16 B): composite key (forced <=>
+// bit 63 clear), KV blocks, (id_base + slot) | running << 31.
+struct RkItem {
+  unsigned long long key;
+  uint32_t kv;
+  uint32_t gid;
+};
+
 __global__ void __launch_bounds__(kT)
 trail_select_rank_kernel(const Record *__restrict__ rec_in, Record *__restrict__ rec_out,
                          const uint32_t *__restrict__ ids, const uint32_t *__restrict__ arrival,
                          const int32_t *__restrict__ kv, const uint8_t *__restrict__ running,
                          const SlotMeta *__restrict__ meta, const HeadConsts *__restrict__ cst,
                          int max_slots, uint32_t id_base, uint32_t *__restrict__ err, int n,
-                         long long budget, int max_run, Record *__restrict__ sorted,
-                         uint32_t *__restrict__ done_cnt, uint32_t *__restrict__ run_ids,
-                         uint32_t *__restrict__ pre_ids, uint32_t *__restrict__ adm_ids,
-                         int32_t *__restrict__ counts) {
-  extern __shared__ unsigned long long skey[];   // [n]
+                         int ipc_log2, long long budget, int max_run,
+                         uint2 *__restrict__ scratch, uint32_t *__restrict__ gcnt,
+                         uint32_t *__restrict__ run_ids, uint32_t *__restrict__ pre_ids,
+                         uint32_t *__restrict__ adm_ids, int32_t *__restrict__ counts,
+                         uint64_t *__restrict__ trace) {
+  extern __shared__ RkItem sitem[];   // [n]
   __shared__ RkShared sh;
-  const int tid = threadIdx.x, lane = tid & 31;
+  __shared__ unsigned long long s_part[kT / 32][3];
+  __shared__ uint32_t s_cta_run, s_cta_rcut;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t *tr = trace ? trace + 16 * (int64_t)blockIdx.x : nullptr;   // diagnostics
+  if (tr && tid == 0) tr[0] = ptx::gtimer();
   griddep_wait();     // slot state from the predict kernels
   griddep_launch();
+  if (tr && tid == 0) tr[1] = ptx::gtimer();
+  if (tid == 0) { s_cta_run = 0u; s_cta_rcut = 0u; }
 
-  // 1. all n composite keys -> shared memory; count the valid (non-padding) records
-  int my_valid = 0;
+  // 1. every record's key, kv and flags -> shared memory; forced count / KV, running count
+  long long fkv_t = 0;
+  int f_t = 0, r_t = 0, v_t = 0;
   for (int j = tid; j < n; j += kT) {
-    Record r = rec_in ? rec_in[j]
-                      : rk_make_record(j, ids, arrival, kv, running, meta, cst, max_slots,
-                                       id_base, err, blockIdx.x == 0);
-    const unsigned long long kk = rk_key(r);
-    skey[j] = kk;
-    my_valid += kk != ~0ull ? 1 : 0;
+    const Record r = rec_in ? rec_in[j]
+                            : rk_make_record(j, ids, arrival, kv, running, meta, cst, max_slots,
+                                             id_base, err, blockIdx.x == 0);
+    RkItem it;
+    it.key = rk_key(r);
+    const bool valid = it.key != ~0ull;
+    const bool forced = valid && (r.keybits >> 31) == 0u;
+    const bool runn = valid && (r.gid >> 31) != 0u;
+    it.kv = valid ? r.kv : 0u;
+    it.gid = valid ? r.gid : 0u;
+    sitem[j] = it;
+    v_t += valid ? 1 : 0;
+    f_t += forced ? 1 : 0;
+    r_t += runn ? 1 : 0;
+    fkv_t += forced ? (long long)r.kv : 0;
   }
   {
-    long long a = 0, b = 0;
-    int x = my_valid, y = 0, z = 0;
-    rk_scan(sh, a, b, x, y, z);     // (also the barrier that publishes skey)
+    long long a = fkv_t, b = 0;
+    int x = v_t, y = f_t, z = r_t;
+    rk_scan(sh, a, b, x, y, z);     // totals only (also publishes sitem)
   }
-  const int nv = sh.tc0;
+  const int nv = sh.tc0, nf = sh.tc1, R_total = sh.tc2;
+  const long long Sf = sh.tv0;
+  const int cap = max_run > 0 ? max_run : nv;
+  const bool over = Sf > budget || nf > cap;   // D-16: run = forced only
+  if (tr && tid == 0) tr[2] = ptx::gtimer();
 
-  // 2. exact rank of my records: 8 threads per record, each counting 1/8 of the keys
-  {
-    const int a = blockIdx.x * kItems + (tid >> 3), part = tid & 7;
-    const bool have = a < n;
-    const unsigned long long ka = have ? skey[a] : ~0ull;
-    int cnt = 0;
-    if (have && ka != ~0ull) {
-      int j = part;
-      for (; j + 24 < n; j += 32) {
-        const unsigned long long k0 = skey[j], k1 = skey[j + 8], k2 = skey[j + 16],
-                                 k3 = skey[j + 24];
-        cnt += (k0 < ka || (k0 == ka && j < a)) ? 1 : 0;
-        cnt += (k1 < ka || (k1 == ka && j + 8 < a)) ? 1 : 0;
-        cnt += (k2 < ka || (k2 == ka && j + 16 < a)) ? 1 : 0;
-        cnt += (k3 < ka || (k3 == ka && j + 24 < a)) ? 1 : 0;
-      }
-      for (; j < n; j += 8) {
-        const unsigned long long k0 = skey[j];
-        cnt += (k0 < ka || (k0 == ka && j < a)) ? 1 : 0;
+  // 2. for each of my records: position in the order, cumulative KV through it, running
+  //    records before it — one pass over all keys, TPI threads per record
+  const int ipc = 1 << ipc_log2, tpi = kT >> ipc_log2;
+  const int li = tid / tpi, part = tid % tpi;
+  const int i = blockIdx.x * ipc + li;
+  const bool have = i < n;
+  const RkItem me = have ? sitem[i] : RkItem{~0ull, 0u, 0u};
+  const bool mine = have && me.key != ~0ull;
+  unsigned long long cnt = 0, cum = 0, rb = 0;
+  if (mine) {
+    const unsigned long long ki = me.key;
+    for (int j = part; j < n; j += tpi) {
+      const RkItem o = sitem[j];
+      const bool less = o.key < ki || (o.key == ki && j < i);
+      if (less) {
+        cnt += 1;
+        cum += o.kv;
+        rb += o.gid >> 31;
       }
     }
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 1);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 2);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, 4);
-    if (have && part == 0 && ka != ~0ull) {
-      const Record r = rec_in ? rec_in[a]
-                              : rk_make_record(a, ids, arrival, kv, running, meta, cst,
-                                               max_slots, id_base, err, false);
-      sorted[cnt] = r;
-      if (!rec_in && rec_out) rec_out[a] = r;
+  }
+  // reduce over the tpi threads of a record (consecutive threads)
+  const int wl = tpi < 32 ? tpi : 32;
+  for (int o = 1; o < wl; o <<= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    cum += __shfl_xor_sync(0xffffffffu, cum, o);
+    rb += __shfl_xor_sync(0xffffffffu, rb, o);
+  }
+  if (tpi > 32) {
+    if (lane == 0) { s_part[warp][0] = cnt; s_part[warp][1] = cum; s_part[warp][2] = rb; }
+    __syncthreads();
+    if (part == 0) {
+      const int w0 = tid >> 5, nw = tpi >> 5;
+      cnt = 0; cum = 0; rb = 0;
+      for (int q = 0; q < nw; ++q) {
+        cnt += s_part[w0 + q][0]; cum += s_part[w0 + q][1]; rb += s_part[w0 + q][2];
+      }
     }
   }
-
-  // 3. the last CTA to finish runs the linear part
-  __threadfence();
+  if (mine && part == 0) {
+    const int pos = (int)cnt;
+    const bool forced = (me.key >> 63) == 0ull;
+    const bool runn = (me.gid >> 31) != 0u;
+    const long long cum_incl = (long long)cum + me.kv;
+    const bool in_run = forced ? true : (!over && cum_incl <= budget && pos < cap);
+    const uint32_t gid = me.gid & 0x7FFFFFFFu;
+    if (in_run) {
+      run_ids[pos] = gid;
+      if (!runn) adm_ids[pos - (int)rb] = gid;   // waiting records before pos: pos - rb
+      atomicAdd(&s_cta_run, 1u);
+      if (runn) atomicAdd(&s_cta_rcut, 1u);
+    }
+    scratch[pos] = make_uint2(me.gid, (uint32_t)rb);
+    if (!rec_in && rec_out) {
+      Record r;
+      r.keybits = (uint32_t)(me.key >> 32);
+      r.arrival = (uint32_t)me.key;
+      r.kv = me.kv;
+      r.gid = me.gid;
+      rec_out[i] = r;
+    }
+  }
   __syncthreads();
+  if (tr && tid == 0) tr[3] = ptx::gtimer();
+
+  // 3. per-CTA totals, then the last CTA writes the preempt list (positions need R(cut))
   if (tid == 0) {
-    const uint32_t old = atomicAdd(done_cnt, 1u);
-    const bool last = old == gridDim.x - 1;
-    if (last) *done_cnt = 0u;       // re-arm for the next launch
-    sh.last = last ? 1 : 0;
+    if (s_cta_run) atomicAdd(gcnt + 1, s_cta_run);
+    if (s_cta_rcut) atomicAdd(gcnt + 2, s_cta_rcut);
+    __threadfence();
+    const uint32_t old = atomicAdd(gcnt, 1u);
+    sh.last = old == gridDim.x - 1 ? 1 : 0;
   }
   __syncthreads();
+  if (tr && tid == 0) { tr[4] = ptx::gtimer(); tr[14] = sh.last; }
   if (!sh.last) return;
   __threadfence();
-
-  // blocked arrangement: thread t owns sorted positions [t*E, t*E + E)
-  uint32_t kvv[E], gidv[E];
-  unsigned fmask = 0u, rmask = 0u;
-  long long kv_t = 0, fkv_t = 0;
-  int f_t = 0, r_t = 0;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int p = tid * E + e;
-    kvv[e] = 0u;
-    gidv[e] = 0u;
-    if (p < nv) {
-      const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(sorted + p));
-      kvv[e] = v.z;
-      gidv[e] = v.w;
-      const bool forced = (v.x >> 31) == 0u;
-      const bool runn = (v.w >> 31) != 0u;
-      fmask |= forced ? 1u << e : 0u;
-      rmask |= runn ? 1u << e : 0u;
-      kv_t += v.z;
-      fkv_t += forced ? v.z : 0u;
-      f_t += forced ? 1 : 0;
-      r_t += runn ? 1 : 0;
-    }
+  const int n_run = (int)__ldcg(gcnt + 1);
+  const int R_cut = (int)__ldcg(gcnt + 2);
+  if (tr && tid == 0) tr[5] = ptx::gtimer();
+  for (int p = n_run + tid; p < nv; p += kT) {
+    const uint2 v = __ldcg(scratch + p);
+    if (v.x >> 31) pre_ids[(int)v.y - R_cut] = v.x & 0x7FFFFFFFu;
   }
-  long long kv_off = kv_t, fkv_dummy = fkv_t;
-  int f_off = f_t, r_off = r_t, z_dummy = 0;
-  rk_scan(sh, kv_off, fkv_dummy, f_off, r_off, z_dummy);
-  const long long Sf = sh.tv1;       // KV of the forced set (the sorted prefix [0, nf))
-  const int nf = sh.tc0;
-  const int R_total = sh.tc1;        // running requests among the valid records
-  // non-forced positions whose cumulative KV fits: a prefix (cumulative KV is monotone)
-  int fit_t = 0;
-  {
-    long long cum = kv_off;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int p = tid * E + e;
-      if (p < nv) {
-        cum += kvv[e];
-        if (!(fmask >> e & 1u) && cum <= budget) ++fit_t;
-      }
-    }
-  }
-  const int cap = max_run > 0 ? max_run : nv;
-  int n_run, status;
-  {
-    long long a = 0, b = 0;
-    int x = fit_t, y = 0, z = 0;
-    rk_scan(sh, a, b, x, y, z);
-    const int n_fit = sh.tc0;
-    if (Sf > budget || nf > cap) { n_run = nf; status = TRAIL_WARN_OVER_BUDGET; }
-    else { n_run = min(nf + n_fit, cap); status = TRAIL_OK; }
-  }
-  // running requests before the cut, R(n_run)
-  int R_cut;
-  {
-    int rb_t = 0;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int p = tid * E + e;
-      if (p < nv && p < n_run && (rmask >> e & 1u)) ++rb_t;
-    }
-    long long a = 0, b = 0;
-    int x = rb_t, y = 0, z = 0;
-    rk_scan(sh, a, b, x, y, z);
-    R_cut = sh.tc0;
-  }
-  {
-    int rp = r_off;                  // running requests at sorted positions < p
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int p = tid * E + e;
-      if (p < nv) {
-        const bool runn = (rmask >> e & 1u) != 0u;
-        const uint32_t gid = gidv[e] & 0x7FFFFFFFu;
-        if (p < n_run) {
-          run_ids[p] = gid;
-          if (!runn) adm_ids[p - rp] = gid;     // waiting requests before p: p - rp
-        } else if (runn) {
-          pre_ids[rp - R_cut] = gid;
-        }
-        rp += runn ? 1 : 0;
-      }
-    }
-  }
+  if (tr && tid == 0) tr[6] = ptx::gtimer();
+  __syncthreads();
   if (tid == 0) {
     counts[0] = n_run;
     counts[1] = R_total - R_cut;
     counts[2] = n_run - R_cut;
-    counts[3] = status;
+    counts[3] = over ? TRAIL_WARN_OVER_BUDGET : TRAIL_OK;
+    gcnt[0] = 0u; gcnt[1] = 0u; gcnt[2] = 0u;      // re-arm for the next launch
   }
+  if (tr && tid == 0) tr[7] = ptx::gtimer();
   (void)lane;
-  (void)fkv_dummy;
-  (void)z_dummy;
 }
 
 // ------------------------------------------------------------------ host
 int select_rank_capacity() { return kRankCap; }
 
 cudaError_t select_rank_prepare() {
-  cudaError_t e = cudaSuccess;
-#define RK_ATTR(EE)                                                                     \
-  if (e == cudaSuccess)                                                                 \
-    e = cudaFuncSetAttribute(trail_select_rank_kernel<EE>,                              \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, kRankCap * 8);
-  RK_ATTR(1) RK_ATTR(2) RK_ATTR(4) RK_ATTR(8) RK_ATTR(16)
-#undef RK_ATTR
-  return e;
+  return cudaFuncSetAttribute(trail_select_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kRankCap * (int)sizeof(RkItem));
 }
 
 cudaError_t launch_select_rank(const Ctx &c, const Record *rec_in, Record *rec_out,
@@ -322,19 +309,20 @@ cudaError_t launch_select_rank(const Ctx &c, const Record *rec_in, Record *rec_o
                                uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
                                cudaStream_t s) {
   if (n > kRankCap || !c.rank_sorted || !c.rank_cnt) return cudaErrorInvalidValue;
-  const int grid = n > 0 ? (n + kItems - 1) / kItems : 1;
-  const size_t smem = (size_t)n * 8;
-#define RK_LAUNCH(EE)                                                                         \
-  return launch_k(trail_select_rank_kernel<EE>, dim3(grid), dim3(kT), smem, s, rec_in, rec_out, \
-                  ids, arrival, kv, running, (const SlotMeta *)c.meta,                        \
-                  (const HeadConsts *)c.consts, c.cfg.max_slots, c.cfg.id_base, c.dev_err, n, \
-                  (long long)budget, max_run, c.rank_sorted, c.rank_cnt, run, pre, adm, counts)
-  if (n <= kT) RK_LAUNCH(1);
-  if (n <= 2 * kT) RK_LAUNCH(2);
-  if (n <= 4 * kT) RK_LAUNCH(4);
-  if (n <= 8 * kT) RK_LAUNCH(8);
-  RK_LAUNCH(16);
-#undef RK_LAUNCH
+  // records per CTA: a power of two spreading the n records over about one wave of SMs,
+  // with at least 8 threads per record
+  int ipc_log2 = 0;
+  while ((1 << ipc_log2) * c.num_sms < n && ipc_log2 < 6) ++ipc_log2;
+  const int ipc = 1 << ipc_log2;
+  const int grid = n > 0 ? (n + ipc - 1) / ipc : 1;
+  const size_t smem = (size_t)std::max(n, 1) * sizeof(RkItem);
+  return launch_k(trail_select_rank_kernel, dim3(grid), dim3(kT), smem, s, rec_in, rec_out, ids,
+                  arrival, kv, running, (const SlotMeta *)c.meta, (const HeadConsts *)c.consts,
+                  c.cfg.max_slots, c.cfg.id_base, c.dev_err, n, ipc_log2, (long long)budget,
+                  max_run, reinterpret_cast<uint2 *>(c.rank_sorted), c.rank_cnt, run, pre, adm,
+                  counts,
+                  (c.trace && grid <= c.trace_cap && getenv("TRAIL_TRACE_SELECT")) ? c.trace
+                                                                                   : nullptr);
 }
 
 }  // namespace trail

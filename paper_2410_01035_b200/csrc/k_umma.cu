@@ -240,18 +240,24 @@ static PFN_encodeTiled get_encode() {
   return fn;
 }
 
-static bool encode_2d_bf16(CUtensorMap *m, const void *base, uint64_t inner, uint64_t outer,
-                           uint32_t box_inner, uint32_t box_outer) {
+// bf16 row-major [rows][ld] (cols used), SWIZZLE_128B boxes of box_cols x box_rows
+bool encode_rows_bf16(CUtensorMap *m, const void *base, uint64_t cols, uint64_t rows, uint64_t ld,
+                      uint32_t box_cols, uint32_t box_rows) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {inner * 2};
-  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides,
                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+static bool encode_2d_bf16(CUtensorMap *m, const void *base, uint64_t inner, uint64_t outer,
+                           uint32_t box_inner, uint32_t box_outer) {
+  return encode_rows_bf16(m, base, inner, outer, inner, box_inner, box_outer);
 }
 
 cudaError_t umma_prepare(Ctx &c) {
@@ -260,6 +266,11 @@ cudaError_t umma_prepare(Ctx &c) {
       !encode_2d_bf16(&c.tmap_w128, c.w1, (uint64_t)c.d, (uint64_t)c.H, BK, 128) ||
       (c.H % 256 == 0 &&
        !encode_2d_bf16(&c.tmap_w256, c.w1, (uint64_t)c.d, (uint64_t)c.H, BK, 256)))
+    return cudaErrorInvalidValue;
+  const uint64_t xr = (uint64_t)c.cfg.max_requests;
+  if (!encode_rows_bf16(&c.tmap_xs1, c.xs, (uint64_t)c.d, xr, (uint64_t)c.d, BK, 1) ||
+      !encode_rows_bf16(&c.tmap_xs4, c.xs, (uint64_t)c.d, xr, (uint64_t)c.d, BK, 4) ||
+      !encode_rows_bf16(&c.tmap_xs32, c.xs, (uint64_t)c.d, xr, (uint64_t)c.d, BK, 32))
     return cudaErrorInvalidValue;
   c.have_tmaps = true;
   cudaError_t e = cudaFuncSetAttribute(trail_umma_l1_kernel<128>,

@@ -40,6 +40,16 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
 }
+// TMA tile::gather4: four rows (row coordinates r0..r3, column c0) of a 2-D tensor map whose
+// box is (cols x 1) into 4 consecutive box-sized rows of shared memory (swizzle applied).
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, uint32_t bar,
+                                            int c0, int r0, int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
 // Bulk copy of `bytes` (multiple of 16) from this CTA's shared memory into the shared
 // memory of a CTA of the cluster (dst and bar are shared::cluster addresses from mapa);
 // completion is signalled on the destination CTA's mbarrier.

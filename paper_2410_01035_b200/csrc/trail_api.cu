@@ -133,7 +133,7 @@ trail_status set_device(const Ctx &c) {
 void free_ctx(Ctx &c) {
   void *ptrs[] = {c.w1, c.b1, c.w2, c.b2, c.consts, c.lq, c.meta, c.dev_err, c.xs,
                   c.partial, c.rec_local, c.rec_all, c.sel_scratch, c.zpart, c.arrive_cnt, c.trace,
-                  c.rank_sorted, c.rank_cnt};
+                  c.rank_sorted, c.rank_cnt, c.pool_head, c.pool_tail, c.pool_cnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c.prof_ev) {
@@ -197,6 +197,7 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
   if (!g.w1 || !g.b1 || !g.w2 || !g.b2 || !g.bin_edges) return TRAIL_ERR_INVALID;
   if (!(g.c >= 0.0)) return TRAIL_ERR_INVALID;   // rejects NaN and negatives
   if (g.max_slots <= 0 || g.max_requests <= 0 || g.max_sched < 0) return TRAIL_ERR_INVALID;
+  if (g.max_requests > (1 << 18)) return TRAIL_ERR_INVALID;   // K1 offset search bound
   if (g.world_size < 1) return TRAIL_ERR_INVALID;
   if (g.l1_mode < 0 || g.l1_mode > 3) return TRAIL_ERR_INVALID;
   if (g.l1_mode >= TRAIL_L1_UMMA && g.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
@@ -284,6 +285,11 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
   const int max_sched = std::max(1, g.max_sched);
   ALLOC(c.rec_local, (size_t)max_sched * sizeof(Record));
   ALLOC(c.rec_all, (size_t)max_sched * c.world * sizeof(Record));
+  ALLOC(c.pool_head, (size_t)pool_grid(c) * c.d * sizeof(float));
+  ALLOC(c.pool_tail, (size_t)pool_grid(c) * c.d * sizeof(float));
+  ALLOC(c.pool_cnt, (size_t)g.max_requests * sizeof(uint32_t));
+  if (cudaMemset(c.pool_cnt, 0, (size_t)g.max_requests * sizeof(uint32_t)) != cudaSuccess)
+    return fail(TRAIL_ERR_CUDA);
   ALLOC(c.rank_sorted, (size_t)max_sched * c.world * sizeof(Record));
   ALLOC(c.rank_cnt, 16 * sizeof(uint32_t));
   if (cudaMemset(c.rank_cnt, 0, 16 * sizeof(uint32_t)) != cudaSuccess) return fail(TRAIL_ERR_CUDA);
@@ -390,11 +396,12 @@ trail_status trail_predict_step(trail_handle h, const void *emb, int64_t emb_ld,
     return TRAIL_ERR_CAPACITY;
   {
     ProfScope p(c, TRAIL_K_POOL, s);
-    TRAIL_CUDA(launch_pool(c, emb, emb_ld, row_offsets, n, s));
+    TRAIL_CUDA(launch_pool(c, emb, emb_ld, row_offsets, n, mode == TRAIL_L1_UMMA ? 0 : 1, s));
   }
   if (mode == TRAIL_L1_UMMA) {   // layer 1 + layer 2 + head in one kernel
     ProfScope p(c, TRAIL_K_UMMA, s);
-    TRAIL_CUDA(launch_fused_predict(c, n, splits, request_ids, is_prefill, prior_override,
+    TRAIL_CUDA(launch_fused_predict(c, emb, emb_ld, row_offsets, n, splits, request_ids,
+                                    is_prefill, prior_override,
                                     posteriors, expected_remaining, s));
     return TRAIL_OK;
   }

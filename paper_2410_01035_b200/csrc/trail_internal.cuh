@@ -66,6 +66,9 @@ struct Ctx {
   uint64_t *trace = nullptr;   // diagnostics: per-CTA phase timestamps (trail_trace_enable)
   int trace_cap = 0;           // CTAs the trace buffer holds (16 u64 each)
   int fused_max_clusters[17] = {};
+  float *pool_head = nullptr;       // [pool_grid][d] K1 partial sums (request began earlier)
+  float *pool_tail = nullptr;       // [pool_grid][d] K1 partial sums (request continues)
+  uint32_t *pool_cnt = nullptr;     // [max_requests] K1 per-request chunk arrival counters
   Record *rank_sorted = nullptr;    // [max_sched * world] rank-select scatter target
   uint32_t *rank_cnt = nullptr;     // rank-select CTA completion counter  // fused kernel: resident clusters of size s (occupancy)
   Record *rec_local = nullptr; // [max_sched]
@@ -74,6 +77,11 @@ struct Ctx {
   size_t sel_scratch_bytes = 0;
   // TMA descriptors (bf16 path)
   CUtensorMap tmap_x, tmap_w128, tmap_w256;
+  CUtensorMap tmap_xs1, tmap_xs4, tmap_xs32;     // xs rows, boxes 64 x {1, 4, 32} (fused gather)
+  CUtensorMap tmap_emb, tmap_emb4, tmap_emb32;   // caller's embeddings, same boxes; re-encoded
+                                                 // whenever emb / ld change
+  const void *tmap_emb_ptr = nullptr;
+  int64_t tmap_emb_ld = 0;
   bool have_tmaps = false;
   int num_sms = 148;
   // NCCL
@@ -95,8 +103,11 @@ struct Ctx {
 };
 
 // ---------------------------------------------------------------- launchers (host)
+// K1.  write_singles = 0: single-row requests are not copied to xs (the fused tcgen05
+// kernel gathers those rows straight from emb)
 cudaError_t launch_pool(const Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
-                        cudaStream_t s);
+                        int write_singles, cudaStream_t s);
+int pool_grid(const Ctx &c);
 cudaError_t launch_gemv_l1(const Ctx &c, int n, int splits, cudaStream_t s);
 cudaError_t launch_umma_l1(const Ctx &c, int n, int bn, int splits, cudaStream_t s);
 cudaError_t launch_head(const Ctx &c, int n, int splits, const uint32_t *ids,
@@ -111,11 +122,14 @@ cudaError_t launch_select(const Ctx &c, const Record *rec, int n, int64_t budget
 cudaError_t launch_release(const Ctx &c, const uint32_t *ids, int n, cudaStream_t s);
 cudaError_t launch_read_state(const Ctx &c, const uint32_t *ids, int n, float *L, uint32_t *age,
                               uint32_t *thr, uint8_t *seen, float *post, cudaStream_t s);
-cudaError_t umma_prepare(Ctx &c);                // encode tensor maps, set smem attributes
+cudaError_t umma_prepare(Ctx &c);
+bool encode_rows_bf16(CUtensorMap *m, const void *base, uint64_t cols, uint64_t rows, uint64_t ld,
+                      uint32_t box_cols, uint32_t box_rows);                // encode tensor maps, set smem attributes
 int umma_max_bn(const Ctx &c);
 cudaError_t fused_prepare(Ctx &c);
 int fused_splits(const Ctx &c, int n);
-cudaError_t launch_fused_predict(const Ctx &c, int n, int splits, const uint32_t *ids,
+cudaError_t launch_fused_predict(Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
+                                 int splits, const uint32_t *ids,
                                  const uint8_t *is_prefill, const float *prior_override,
                                  float *post, float *L, cudaStream_t s);
 cudaError_t select_prepare(Ctx &c);
