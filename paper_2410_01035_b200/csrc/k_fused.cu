@@ -44,7 +44,6 @@ constexpr int THREADS = 256;
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int BK = 64;
-constexpr int STAGES = 6;
 constexpr int MAXS = 16;                              // max cluster size along K
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;
@@ -53,115 +52,125 @@ constexpr int TILE_LD = BN + 4;                       // padded fp32 row stride 
 constexpr int ROW_BYTES = TILE_LD * 4;
 constexpr int TILE_BYTES = BM * ROW_BYTES;            // 67584
 constexpr int LAND_OFF = TILE_BYTES;                  // landing slots for peers' row groups
-constexpr int PIPE_BYTES = STAGES * STAGE_BYTES;      // 192 KB, reused by tile + landing
-constexpr int BAR_OFF = PIPE_BYTES;
-constexpr int W2_OFF = PIPE_BYTES + 256;
-constexpr int W2_FLOATS = kMaxBins * BN;
-constexpr int SMEM_USED = W2_OFF + (W2_FLOATS + BN) * 4;
-constexpr int SMEM_TOTAL = SMEM_USED + 1024;          // + slack for 1024-byte alignment
-static_assert(LAND_OFF + (BM + MAXS) * ROW_BYTES <= PIPE_BYTES, "tile + landing must fit");
 
-__device__ __forceinline__ float logaddexp_f(float a, float b) {
-  const float mx = fmaxf(a, b), mn = fminf(a, b);
-  if (mx == -INFINITY) return -INFINITY;
-  return mx + log1pf(expf(mn - mx));
-}
+// Shared-memory plan (KB = bin bound): pipeline stages (reused by the partial tile and the
+// landing slots after the mainloop), barriers, W2 / b1 slices, and the per-row slot state
+// of the rows this CTA may run the head for (prefetched during the mainloop).
+template <int KB>
+struct FCfg {
+  static constexpr int STAGES = KB <= 20 ? 6 : 5;
+  static constexpr int PIPE_BYTES = STAGES * STAGE_BYTES;
+  static constexpr int BAR_OFF = PIPE_BYTES;
+  static constexpr int W2_OFF = BAR_OFF + 256;
+  static constexpr int B1_OFF = W2_OFF + KB * BN * 4;
+  static constexpr int SLOT_OFF = B1_OFF + BN * 4;     // u32 [BM]: slot id | prefill << 31
+  static constexpr int META_OFF = SLOT_OFF + BM * 4;   // SlotMeta [BM]
+  static constexpr int LQ_OFF = META_OFF + BM * 16;    // float [BM][KB] previous log q
+  static constexpr int HC_OFF = LQ_OFF + BM * KB * 4;   // HeadSmem (per-bin constants)
+  static constexpr int SMEM_USED = HC_OFF + 5 * kMaxBins * 4;
+  static constexpr int SMEM_TOTAL = SMEM_USED + 1024;  // + slack for 1024-byte alignment
+  static_assert(LAND_OFF + (BM + MAXS) * ROW_BYTES <= PIPE_BYTES, "tile + landing must fit");
+  static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
+};
+
 __host__ __device__ __forceinline__ int row_lo(int r, int S) { return (r * BM) / S; }
 }  // namespace
 
-// One request's head in one thread (all bins in registers, KB >= k compile-time bound).
-template <int KB>
-__device__ __forceinline__ void head_one(int j, const float (&z)[KB] /* incl. b2 */, int k,
-                                         const HeadConsts *__restrict__ cst,
-                                         const uint32_t *__restrict__ ids,
-                                         const uint8_t *__restrict__ is_prefill,
-                                         const float *__restrict__ prior_override, int max_slots,
-                                         float *__restrict__ lq_state,
-                                         SlotMeta *__restrict__ meta, float *__restrict__ post,
-                                         float *__restrict__ Lout, uint32_t *__restrict__ err) {
-  const uint32_t slot = __ldg(ids + j);
-  if (slot >= (uint32_t)max_slots) {
-    atomicOr(err, TRAIL_DEV_BAD_ID);
-    if (post)
-      for (int b = 0; b < k; ++b) post[(int64_t)j * k + b] = NAN;
-    if (Lout) Lout[j] = NAN;
+// Per-bin constants of the head, staged in shared memory (lane b reads entry b).
+struct HeadSmem {
+  float m[kMaxBins], log_stay[kMaxBins], log_move[kMaxBins], log_prior[kMaxBins];
+  uint32_t thr[kMaxBins];
+};
+
+__device__ __forceinline__ float seg_max(float v, int seg) {
+  for (int o = seg >> 1; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o, seg));
+  return v;
+}
+__device__ __forceinline__ float seg_sum(float v, int seg) {
+  for (int o = seg >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, seg);
+  return v;
+}
+
+// Row a3 head for request j, one lane per bin (b) in a SEG-lane segment; every lane of the
+// warp calls it (j >= n: inactive segment, shuffles only).  Log-domain recursion (D-22) with
+// fast-math exp/log (MUFU, ~2 ulp: errors ~1e-7, far inside the 2e-3 posterior bound).
+//   log p = z - logsumexp(z)                                   (softmax)
+//   prefill: log q = log pi + log p                            (D-9 threshold)
+//   decode:  log q = logaddexp(log T_bb + lq(b), log T_b,b+1 + lq(b+1)) + log p
+//   normalise; L = sum_b q(b) m_b
+// Five segment reductions: max z, sum exp, (max, argmax) of the unnormalised log q, sum exp,
+// sum q m.  The D-5 fallback (all-zero product) needs max log p = max z - lse: no reduction.
+__device__ __forceinline__ void head_seg(int j, int n, int k, int SEG, int b, float z,
+                                         const HeadSmem &hc, uint32_t sl, const SlotMeta &mt,
+                                         float lq_prev, const float *__restrict__ prior_override,
+                                         float *__restrict__ lq_state, SlotMeta *__restrict__ meta,
+                                         float *__restrict__ post, float *__restrict__ Lout,
+                                         uint32_t *__restrict__ err) {
+  const bool act = j < n && b < k;
+  const bool bad = sl == 0xFFFFFFFFu;
+  const uint32_t slot = sl & 0x7FFFFFFFu;
+  if (!act) z = -INFINITY;
+  const float zmax = seg_max(z, SEG);
+  const float lse = zmax + __logf(seg_sum(act ? __expf(z - zmax) : 0.f, SEG));
+  const float lp = act ? z - lse : -INFINITY;
+  const bool first = (sl >> 31) != 0u || !(mt.flags & 1u);
+  const float prev = (act && !first && !bad) ? lq_prev : -INFINITY;
+  float prev1 = __shfl_down_sync(0xffffffffu, prev, 1, SEG);
+  if (b + 1 >= k) prev1 = -INFINITY;
+  float lq = -INFINITY;
+  if (act) {
+    float lpr;
+    if (first) {
+      lpr = prior_override ? __logf(__ldg(prior_override + (int64_t)j * k + b)) : hc.log_prior[b];
+    } else {
+      // prior(b) = (1 - 1/w_b) q(b) + (1/w_{b+1}) q(b+1): T applied to the posterior (D-1, D-2)
+      const float stay = hc.log_stay[b] + prev, move = hc.log_move[b] + prev1;
+      const float mx = fmaxf(stay, move), mn = fminf(stay, move);
+      lpr = mx == -INFINITY ? -INFINITY : mx + __logf(1.f + __expf(mn - mx));
+    }
+    lq = lpr + lp;
+  }
+  // (max, argmax) of the unnormalised log q, lowest index on ties (argmax of q^(0), D-9)
+  float qmax = lq;
+  int bi = act ? b : 0x7FFFFFFF;
+  for (int o = SEG >> 1; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, qmax, o, SEG);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o, SEG);
+    if (ov > qmax || (ov == qmax && oi < bi)) { qmax = ov; bi = oi; }
+  }
+  if (qmax == -INFINITY) {          // all-zero product: fall back to p (D-5)
+    lq = lp;
+    qmax = zmax - lse;
+    bi = 0;                         // (only reachable for a zero prior on every bin)
+  }
+  const float qs = seg_sum(act ? __expf(lq - qmax) : 0.f, SEG);   // every lane shuffles
+  lq = act ? lq - (qmax + __logf(qs)) : -INFINITY;
+  const float q = act ? __expf(lq) : 0.f;
+  const float L = seg_sum(act ? q * hc.m[b] : 0.f, SEG);
+  if (j >= n) return;
+  if (bad) {
+    if (b == 0) atomicOr(err, TRAIL_DEV_BAD_ID);
+    if (b < k && post) post[(int64_t)j * k + b] = NAN;
+    if (b == 0 && Lout) Lout[j] = NAN;
     return;
   }
-  // log p = z - logsumexp(z)
-  float zmax = -INFINITY;
-#pragma unroll
-  for (int b = 0; b < KB; ++b)
-    if (b < k) zmax = fmaxf(zmax, z[b]);
-  float se = 0.f;
-#pragma unroll
-  for (int b = 0; b < KB; ++b)
-    if (b < k) se += expf(z[b] - zmax);
-  const float lse = zmax + logf(se);
-  SlotMeta mt = meta[slot];
-  const bool first = (__ldg(is_prefill + j) != 0) || !(mt.flags & 1u);
-  float lq[KB];
-  if (first) {
-#pragma unroll
-    for (int b = 0; b < KB; ++b)
-      if (b < k)
-        lq[b] = (z[b] - lse) + (prior_override ? logf(__ldg(prior_override + (int64_t)j * k + b))
-                                               : cst->log_prior[b]);
-  } else {
-    float prev[KB];
-#pragma unroll
-    for (int b = 0; b < KB; ++b)
-      if (b < k) prev[b] = lq_state[(int64_t)slot * k + b];
-#pragma unroll
-    for (int b = 0; b < KB; ++b) {
-      if (b < k) {
-        // prior(b) = (1 - 1/w_b) q(b) + (1/w_{b+1}) q(b+1): T applied to the posterior
-        const float stay = cst->log_stay[b] + prev[b];
-        const float move = (b + 1 < k) ? cst->log_move[b] + prev[(b + 1) % KB] : -INFINITY;
-        lq[b] = logaddexp_f(stay, move) + (z[b] - lse);
-      }
+  if (b < k) {
+    lq_state[(int64_t)slot * k + b] = lq;
+    if (post) post[(int64_t)j * k + b] = q;
+  }
+  if (b == 0) {
+    SlotMeta o = mt;
+    if (first) {
+      o.thr = hc.thr[bi];
+      o.age = 0;
+      o.flags = 1u;
+    } else {
+      o.age += 1;
     }
+    o.L = L;
+    meta[slot] = o;
+    if (Lout) Lout[j] = L;
   }
-  float qmax = -INFINITY;
-#pragma unroll
-  for (int b = 0; b < KB; ++b)
-    if (b < k) qmax = fmaxf(qmax, lq[b]);
-  if (qmax == -INFINITY) {          // all-zero product: fall back to p (D-5)
-#pragma unroll
-    for (int b = 0; b < KB; ++b)
-      if (b < k) {
-        lq[b] = z[b] - lse;
-        qmax = fmaxf(qmax, lq[b]);
-      }
-  }
-  float qs = 0.f;
-#pragma unroll
-  for (int b = 0; b < KB; ++b)
-    if (b < k) qs += expf(lq[b] - qmax);
-  const float lnorm = qmax + logf(qs);
-  float L = 0.f;
-  int amax = 0;
-  float best = -INFINITY;
-#pragma unroll
-  for (int b = 0; b < KB; ++b) {
-    if (b < k) {
-      lq[b] -= lnorm;
-      const float q = expf(lq[b]);
-      L = fmaf(q, cst->m[b], L);
-      if (lq[b] > best) { best = lq[b]; amax = b; }    // lowest index on ties
-      lq_state[(int64_t)slot * k + b] = lq[b];
-      if (post) post[(int64_t)j * k + b] = q;
-    }
-  }
-  if (first) {
-    mt.thr = cst->thr_tab[amax];
-    mt.age = 0;
-    mt.flags = 1u;
-  } else {
-    mt.age += 1;
-  }
-  mt.L = L;
-  meta[slot] = mt;
-  if (Lout) Lout[j] = L;
 }
 
 template <int KB>
@@ -175,22 +184,27 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
                            const __grid_constant__ CUtensorMap tmap_w,
                            const int32_t *__restrict__ off, int n, int H, int kblocks,
                            int splits, const float *__restrict__ b1, const float *__restrict__ w2,
-                           const float *__restrict__ b2, const HeadConsts *__restrict__ cst,
+                           const float *__restrict__ b2, const __grid_constant__ HeadConsts cst,
                            float *__restrict__ zpart, uint32_t *__restrict__ arrive_cnt,
                            const uint32_t *__restrict__ ids, const uint8_t *__restrict__ is_prefill,
                            const float *__restrict__ prior_override, int max_slots,
                            float *__restrict__ lq_state, SlotMeta *__restrict__ meta,
                            float *__restrict__ post, float *__restrict__ Lout,
                            uint32_t *__restrict__ err, uint64_t *__restrict__ trace) {
+  using C = FCfg<KB>;
+  constexpr int STAGES = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the SW128 operand tiles; offsetting the __shared__ array (not
   // casting through an integer) keeps every epilogue access an LDS/STS, not a generic LD/ST
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + BAR_OFF);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + BAR_OFF + 8 * (2 * STAGES + 2));
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::BAR_OFF);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::BAR_OFF + 8 * (2 * STAGES + 2));
   uint32_t *flag = tmem_slot + 1;
-  float *w2s = reinterpret_cast<float *>(smem + W2_OFF);   // [KB][BN], rows >= k zero
-  float *b1s = w2s + W2_FLOATS;                            // [BN]
+  float *w2s = reinterpret_cast<float *>(smem + C::W2_OFF);   // float4 [BN/4][KB], b >= k zero
+  float *b1s = reinterpret_cast<float *>(smem + C::B1_OFF);   // [BN]
+  uint32_t *s_slot = reinterpret_cast<uint32_t *>(smem + C::SLOT_OFF);
+  SlotMeta *s_meta = reinterpret_cast<SlotMeta *>(smem + C::META_OFF);
+  float *s_lq = reinterpret_cast<float *>(smem + C::LQ_OFF);
   float *tile = reinterpret_cast<float *>(smem);           // [BM][TILE_LD] after the mainloop
   const uint32_t sA0 = smem_u32(smem), sB0 = sA0 + STAGES * A_BYTES;
   const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * STAGES;
@@ -208,7 +222,7 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
   const int m0 = blockIdx.x * BM, nt = blockIdx.y, n0 = nt * BN, NT = gridDim.y;
   const int S = splits;
   const int crank = S > 1 ? (int)cluster_rank() : 0;
-  const int k = cst->k;
+  const int k = cst.k;
   const int kb0 = (int)((int64_t)crank * kblocks / S);
   const int kb1 = (int)((int64_t)(crank + 1) * kblocks / S);
   const int nkb = kb1 - kb0;
@@ -354,12 +368,40 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
         const int b = v / (BN / 4), c = (v % (BN / 4)) * 4;
         float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
         if (b < k) w = __ldg(reinterpret_cast<const float4 *>(w2 + (int64_t)b * H + n0 + c));
-        *reinterpret_cast<float4 *>(w2s + b * BN + c) = w;
+        reinterpret_cast<float4 *>(w2s)[(c >> 2) * KB + b] = w;   // w2q[c/4][b] = W2[b][c..c+3]
       }
     }
     if (t < BN / 4)
       *reinterpret_cast<float4 *>(b1s + 4 * t) =
           __ldg(reinterpret_cast<const float4 *>(b1 + n0 + 4 * t));
+    if (t < kMaxBins) {
+      HeadSmem &hs = *reinterpret_cast<HeadSmem *>(smem + C::HC_OFF);
+      hs.m[t] = cst.m[t];
+      hs.log_stay[t] = cst.log_stay[t];
+      hs.log_move[t] = cst.log_move[t];
+      hs.log_prior[t] = cst.log_prior[t];
+      hs.thr[t] = cst.thr_tab[t];
+    }
+    // slot state of the rows this CTA may run the head for (no other CTA of this launch
+    // touches those slots; earlier writers completed — PDL chain): off the critical path
+    if (t < rows) {
+      const int j = m0 + r0 + t;
+      uint32_t sl = 0xFFFFFFFFu;
+      if (j < n) {
+        sl = __ldg(ids + j);
+        const bool pref = __ldg(is_prefill + j) != 0;
+        if (sl < (uint32_t)max_slots) {
+          s_meta[t] = meta[sl];
+#pragma unroll
+          for (int b = 0; b < KB; ++b)
+            if (b < k) s_lq[t * KB + b] = lq_state[(int64_t)sl * k + b];
+          sl |= pref ? 0x80000000u : 0u;
+        } else {
+          sl = 0xFFFFFFFFu;
+        }
+      }
+      s_slot[t] = sl;
+    }
   }
 
   // No griddep_wait for the epilogue: it reads only inputs, weights and slot state written by
@@ -407,89 +449,82 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
   }
   if (tr && tid == 0) tr[6] = gtimer();
 
-  // ---- 3. fixed-order sum over the S partials, b1, ReLU, layer-2 partial logits
+  // ---- 3a. h = ReLU(sum of the S partials in rank order + b1) for my rows, in place
+  //           (compact loops: these kernels run once per step, so instruction fetch from
+  //           L2 is on the critical path and straight-line unrolled code costs more than
+  //           it saves)
   {
-    // 32 rows x 8 column lanes per pass; lane cg owns columns 4cg + 32c4 (c4 = 0..3), so the
-    // 8 lanes of a row read 128 contiguous bytes of W2 / the tile: no bank conflicts
-    const int rg = tid >> 3, cg = tid & 7;
-    const int col0 = cg * 4;
     const float *land_f = reinterpret_cast<const float *>(smem + LAND_OFF);
-    for (int rb = 0; rb < rows; rb += THREADS / 8) {
-      const int row = rb + rg;
-      const bool valid = row < rows;
-      const int rr = valid ? row : 0;
-      float zp[KB];
-#pragma unroll
-      for (int b = 0; b < KB; ++b) zp[b] = 0.f;
-#pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
-        const int col = col0 + 32 * c4;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = tid; i < rows * (BN / 4); i += THREADS) {
+      const int r = i >> 5, c = (i & 31) * 4;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int p = 0; p < S; ++p) {
+        const float *src = p == crank ? tile + (r0 + r) * TILE_LD + c
+                                      : land_f + (p * slot_rows + r) * TILE_LD + c;
+        const float4 v = *reinterpret_cast<const float4 *>(src);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      const float4 bb = *reinterpret_cast<const float4 *>(b1s + c);
+      *reinterpret_cast<float4 *>(tile + (r0 + r) * TILE_LD + c) =
+          make_float4(fmaxf(acc.x + bb.x, 0.f), fmaxf(acc.y + bb.y, 0.f),
+                      fmaxf(acc.z + bb.z, 0.f), fmaxf(acc.w + bb.w, 0.f));
+    }
+  }
+  __syncthreads();
+  // ---- 3b. layer-2 partial logits of this column tile, one thread per (row, bin)
+  for (int i = tid; i < rows * KB; i += THREADS) {
+    const int r = i / KB, b = i - r * KB;
+    const int j = m0 + r0 + r;
+    if (b < k && j < n) {
+      const float4 *hr = reinterpret_cast<const float4 *>(tile + (r0 + r) * TILE_LD);
+      const float4 *wq = reinterpret_cast<const float4 *>(w2s) + b;
+      float z0 = 0.f, z1 = 0.f;
 #pragma unroll 4
-        for (int p = 0; p < S; ++p) {
-          const float *src = p == crank ? tile + (r0 + rr) * TILE_LD + col
-                                        : land_f + (p * slot_rows + rr) * TILE_LD + col;
-          const float4 v = *reinterpret_cast<const float4 *>(src);
-          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        }
-        const float4 bb = *reinterpret_cast<const float4 *>(b1s + col);
-        const float h0 = fmaxf(acc.x + bb.x, 0.f), h1 = fmaxf(acc.y + bb.y, 0.f);
-        const float h2 = fmaxf(acc.z + bb.z, 0.f), h3 = fmaxf(acc.w + bb.w, 0.f);
-#pragma unroll
-        for (int b = 0; b < KB; ++b) {
-          const float4 w = *reinterpret_cast<const float4 *>(w2s + b * BN + col);
-          zp[b] = fmaf(w.x, h0, fmaf(w.y, h1, fmaf(w.z, h2, fmaf(w.w, h3, zp[b]))));
-        }
+      for (int c4 = 0; c4 < BN / 4; c4 += 2) {
+        const float4 h0 = hr[c4], w0 = wq[c4 * KB];
+        const float4 h1 = hr[c4 + 1], w1 = wq[(c4 + 1) * KB];
+        z0 = fmaf(h0.x, w0.x, fmaf(h0.y, w0.y, fmaf(h0.z, w0.z, fmaf(h0.w, w0.w, z0))));
+        z1 = fmaf(h1.x, w1.x, fmaf(h1.y, w1.y, fmaf(h1.z, w1.z, fmaf(h1.w, w1.w, z1))));
       }
-#pragma unroll
-      for (int o = 1; o < 8; o <<= 1) {
-#pragma unroll
-        for (int b = 0; b < KB; ++b) zp[b] += __shfl_xor_sync(0xffffffffu, zp[b], o);
-      }
-      const int grow = m0 + r0 + row;
-      if (valid && cg == 0 && grow < n) {
-        float *zo = zpart + ((int64_t)grow * NT + nt) * k;
-#pragma unroll
-        for (int b = 0; b < KB; ++b)
-          if (b < k) zo[b] = zp[b];
-      }
+      zpart[((int64_t)j * NT + nt) * k + b] = z0 + z1;
     }
   }
   if (tr && tid == 0) tr[7] = gtimer();
 
   // ---- 4. last column tile of this row group runs the head
-  __threadfence();
   __syncthreads();
   if (tid == 0) {
     uint32_t *cnt = arrive_cnt + (int64_t)blockIdx.x * MAXS + crank;
-    const uint32_t old = atomicAdd(cnt, 1u);
+    uint32_t old;
+    // release: this CTA's z_part stores (ordered before by the barrier); acquire: the other
+    // column tiles' stores, for the head
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
     const bool last = old == (uint32_t)(NT - 1);
     if (last) *cnt = 0u;                        // re-arm for the next launch
     *flag = last ? 1u : 0u;
   }
   __syncthreads();
+  if (tr && tid == 0) tr[9] = gtimer();
   if (*flag) {
-    __threadfence();
-    if (tid < rows) {
-      const int j = m0 + r0 + tid;
-      if (j < n) {
-        float z[KB];
-#pragma unroll
-        for (int b = 0; b < KB; ++b) z[b] = 0.f;
-        for (int t2 = 0; t2 < NT; ++t2) {       // fixed column-tile order
-          const float *zi = zpart + ((int64_t)j * NT + t2) * k;
-#pragma unroll
-          for (int b = 0; b < KB; ++b)
-            if (b < k) z[b] += __ldcg(zi + b);
-        }
-#pragma unroll
-        for (int b = 0; b < KB; ++b)
-          if (b < k) z[b] += __ldg(b2 + b);
-        head_one<KB>(j, z, k, cst, ids, is_prefill, prior_override, max_slots, lq_state, meta,
-                     post, Lout, err);
+    // one lane per bin, SEG-lane segments (2 requests per warp for k <= 16)
+    const int SEG = k <= 16 ? 16 : 32;
+    const int per_warp = 32 / SEG, seg = lane / SEG, b = lane % SEG;
+    const HeadSmem &hc = *reinterpret_cast<const HeadSmem *>(smem + C::HC_OFF);
+    for (int base = warp * per_warp; base < rows; base += (THREADS / 32) * per_warp) {
+      const int r = base + seg;
+      const int j = r < rows ? m0 + r0 + r : n;
+      float z = 0.f;
+      if (j < n && b < k) {
+        z = __ldg(b2 + b);
+        for (int t = 0; t < NT; ++t) z += __ldcg(zpart + ((int64_t)j * NT + t) * k + b);
       }
+      const int rr = r < rows ? r : 0;
+      head_seg(j, n, k, SEG, b, z, hc, r < rows ? s_slot[r] : 0xFFFFFFFFu, s_meta[rr],
+               b < KB ? s_lq[rr * KB + (b < KB ? b : 0)] : -INFINITY, prior_override, lq_state,
+               meta, post, Lout, err);
     }
   }
+  if (tr && tid == 0) tr[11] = gtimer();
   if (S > 1) cluster_wait();         // every CTA's incoming slices landed: my copies are done
   __syncthreads();
   if (tr && tid == 0) { tr[8] = gtimer(); tr[14] = *flag; }
@@ -500,7 +535,7 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
 template <int KB>
 static cudaError_t fused_attr() {
   cudaError_t e = cudaFuncSetAttribute(trail_fused_predict_kernel<KB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, FCfg<KB>::SMEM_TOTAL);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(trail_fused_predict_kernel<KB>,
                               cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -512,7 +547,7 @@ static cudaError_t fused_occupancy(Ctx &c) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(1, 1, s);
     cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = SMEM_TOTAL;
+    cfg.dynamicSmemBytes = FCfg<KB>::SMEM_TOTAL;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
@@ -583,7 +618,6 @@ cudaError_t launch_fused_predict(Ctx &c, const void *emb, int64_t ld, const int3
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((n + BM - 1) / BM, c.H / BN, splits);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM_TOTAL;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   int na = 0;
@@ -603,11 +637,12 @@ cudaError_t launch_fused_predict(Ctx &c, const void *emb, int64_t ld, const int3
       (c.trace && (int)(cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z) <= c.trace_cap) ? c.trace
                                                                                        : nullptr;
 #define TRAIL_FUSED(KB)                                                                          \
+  cfg.dynamicSmemBytes = FCfg<KB>::SMEM_TOTAL;                                                     \
   return cudaLaunchKernelEx(&cfg, trail_fused_predict_kernel<KB>, c.tmap_emb, c.tmap_emb4,       \
                             c.tmap_emb32, c.tmap_xs1, c.tmap_xs4, c.tmap_xs32,                    \
                             c.tmap_w128, off, n, c.H,                                             \
                             c.d / BK, splits, (const float *)c.b1, (const float *)c.w2,           \
-                            (const float *)c.b2, (const HeadConsts *)c.consts, c.zpart,           \
+                            (const float *)c.b2, c.host_consts, c.zpart,                                  \
                             c.arrive_cnt, ids, is_prefill, prior_override, c.cfg.max_slots, c.lq, \
                             c.meta, post, L, c.dev_err, trace)
   switch (fused_kb(c.k)) {

@@ -37,6 +37,29 @@ __global__ void stamp(uint64_t *out, int idx, int pdl) {
   if (threadIdx.x == 0 && blockIdx.x == 0) out[2 * idx + 1] = gt();
 }
 
+// straight-line code: N independent FMAs on 8 registers, executed once by one warp
+template <int N>
+__global__ void straight(float *out, uint64_t *t) {
+  float a0 = threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+        a6 = a0 + 6, a7 = a0 + 7;
+  uint64_t t0 = gt();
+  a0 += (float)(t0 & 1);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    a0 = fmaf(a0, 1.0001f, 0.5f); a1 = fmaf(a1, 1.0001f, 0.5f); a2 = fmaf(a2, 1.0001f, 0.5f);
+    a3 = fmaf(a3, 1.0001f, 0.5f); a4 = fmaf(a4, 1.0001f, 0.5f); a5 = fmaf(a5, 1.0001f, 0.5f);
+    a6 = fmaf(a6, 1.0001f, 0.5f); a7 = fmaf(a7, 1.0001f, 0.5f);
+  }
+  const float sum = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  uint64_t t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1) : "f"(sum));
+  if (threadIdx.x == 0) { t[0] = t1 - t0; }
+  out[threadIdx.x] = sum;
+}
+__global__ void evict(float *buf, int n) {   // big unrelated kernel + L2 traffic
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) buf[i] += 1.f;
+}
+
 int main() {
   uint64_t *d_out; cudaMalloc(&d_out, 1024 * 8);
   uint64_t h[256];
@@ -80,6 +103,18 @@ int main() {
       printf("graph pdl=%d: kernel start-to-start gaps (ns):", pdl);
       for (int i = 1; i < 8; ++i) printf(" %lld", (long long)(h[2 * i] - h[2 * i - 2]));
       printf("  | first kernel body %lld\n", (long long)(h[1] - h[0]));
+    }
+  }
+  {
+    float *o; cudaMalloc(&o, 4096); float *big; size_t nb = size_t(64) << 20; cudaMalloc(&big, nb * 4);
+    for (int rep = 0; rep < 3; ++rep) {
+      evict<<<592, 256>>>(big, (int)nb); cudaDeviceSynchronize();
+      straight<512><<<1, 32>>>(o, d_out); cudaDeviceSynchronize();
+      cudaMemcpy(h, d_out, 8, cudaMemcpyDeviceToHost); uint64_t cold = h[0];
+      straight<512><<<1, 32>>>(o, d_out); cudaDeviceSynchronize();
+      cudaMemcpy(h, d_out, 8, cudaMemcpyDeviceToHost);
+      printf("straight-line 4096 FMAs (+overhead): cold %llu ns, warm %llu ns\n",
+             (unsigned long long)cold, (unsigned long long)h[0]);
     }
   }
   return 0;

@@ -62,7 +62,10 @@ def main():
             res.append({"ctas": int(len(tr)), "span_ns": int(tr[:, 8].max() - t0),
                         "start_skew_ns": int(tr[:, 0].max() - t0),
                         "sms": int(len(np.unique(tr[:, 15]))),
-                        **{p: [int(np.median(v)), int(v.max())] for p, v in ph.items()}})
+                        **{p: [int(np.median(v)), int(v.max())] for p, v in ph.items()},
+                        "head_ctas": [[int(x) for x in (r[9] - r[7], r[11] - r[9], r[8] - r[11],
+                                                        r[8] - t0)]
+                                      for r in tr[tr[:, 14] == 1][:4]]})
             trail_trace_enable(t.h, 0); trail_trace_enable(t.h, 4096)
         print(json.dumps({"n": args.n, "d": args.d, "splits": int(sp),
                           "dbg": os.environ.get("TRAIL_FUSED_DBG", "0"), "flush": not args.no_flush, "runs": res[2:4]}))
