@@ -90,47 +90,6 @@ __device__ __forceinline__ void rk_scan(RkShared &sh, long long &a, long long &b
   __syncthreads();
 }
 
-// Row a4: the 16-byte record of request i (key L_t or E_pi[L]; forced = running, observed,
-// a >= floor(c r)).  err bits are idempotent (every CTA may set them).
-__device__ __forceinline__ Record rk_make_record(int i, const uint32_t *ids, const uint32_t *arrival,
-                                                 const int32_t *kv, const uint8_t *running,
-                                                 const SlotMeta *meta, const HeadConsts *cst,
-                                                 int max_slots, uint32_t id_base, uint32_t *err,
-                                                 bool flag_errors) {
-  const uint32_t slot = __ldg(ids + i);
-  const bool run = __ldg(running + i) != 0;
-  int32_t kvb = __ldg(kv + i);
-  if (kvb < 0) {
-    if (flag_errors) atomicOr(err, TRAIL_DEV_NEG_KV);
-    kvb = 0;
-  }
-  float key = cst->prior_L;
-  bool forced = false;
-  if (slot < (uint32_t)max_slots) {
-    const SlotMeta m = meta[slot];
-    if (m.flags & 1u) {
-      key = m.L;
-      forced = run && (m.age >= m.thr);
-    }
-  } else {
-    if (flag_errors) atomicOr(err, TRAIL_DEV_BAD_ID);
-    key = INFINITY;
-  }
-  uint32_t kb;
-  if (isfinite(key) && key >= 0.f) {
-    kb = __float_as_uint(key) & 0x7FFFFFFFu;
-  } else {
-    if (flag_errors && slot < (uint32_t)max_slots) atomicOr(err, TRAIL_DEV_NONFIN);
-    kb = 0x7F800000u;
-  }
-  Record r;
-  r.keybits = (forced ? 0u : 0x80000000u) | kb;
-  r.arrival = __ldg(arrival + i);
-  r.kv = (uint32_t)kvb;
-  r.gid = ((id_base + slot) & 0x7FFFFFFFu) | (run ? 0x80000000u : 0u);
-  return r;
-}
-
 __device__ __forceinline__ unsigned long long rk_key(const Record &r) {
   return r.keybits == kPadKey ? ~0ull : ((unsigned long long)r.keybits << 32) | r.arrival;
 }
@@ -162,18 +121,63 @@ trail_select_rank_kernel(const Record *__restrict__ rec_in, Record *__restrict__
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint64_t *tr = trace ? trace + 16 * (int64_t)blockIdx.x : nullptr;   // diagnostics
   if (tr && tid == 0) tr[0] = ptx::gtimer();
+  if (tid == 0) { s_cta_run = 0u; s_cta_rcut = 0u; }
+  // inputs of the local path are the caller's (not produced by the predict kernels): stage
+  // them before waiting on the previous kernel, so only the slot-state loads follow the wait
+  if (!rec_in) {
+    for (int j = tid; j < n; j += kT) {
+      RkItem it;
+      const uint32_t slot = __ldg(ids + j);
+      it.key = __ldg(arrival + j);                       // arrival (low word) for now
+      it.kv = (uint32_t)__ldg(kv + j);
+      it.gid = slot | (__ldg(running + j) ? 0x80000000u : 0u);
+      sitem[j] = it;
+    }
+  }
   griddep_wait();     // slot state from the predict kernels
   griddep_launch();
   if (tr && tid == 0) tr[1] = ptx::gtimer();
-  if (tid == 0) { s_cta_run = 0u; s_cta_rcut = 0u; }
 
   // 1. every record's key, kv and flags -> shared memory; forced count / KV, running count
   long long fkv_t = 0;
   int f_t = 0, r_t = 0, v_t = 0;
   for (int j = tid; j < n; j += kT) {
-    const Record r = rec_in ? rec_in[j]
-                            : rk_make_record(j, ids, arrival, kv, running, meta, cst, max_slots,
-                                             id_base, err, blockIdx.x == 0);
+    Record r;
+    if (rec_in) {
+      r = rec_in[j];
+    } else {   // row a4 from the staged inputs + the slot state
+      const RkItem in = sitem[j];
+      const uint32_t slot = in.gid & 0x7FFFFFFFu;
+      const bool run = (in.gid >> 31) != 0u;
+      int32_t kvb = (int32_t)in.kv;
+      if (kvb < 0) {
+        if (blockIdx.x == 0) atomicOr(err, TRAIL_DEV_NEG_KV);
+        kvb = 0;
+      }
+      float key = cst->prior_L;
+      bool forced = false;
+      if (slot < (uint32_t)max_slots) {
+        const SlotMeta m = meta[slot];
+        if (m.flags & 1u) {
+          key = m.L;
+          forced = run && (m.age >= m.thr);
+        }
+      } else {
+        if (blockIdx.x == 0) atomicOr(err, TRAIL_DEV_BAD_ID);
+        key = INFINITY;
+      }
+      uint32_t kb;
+      if (isfinite(key) && key >= 0.f) {
+        kb = __float_as_uint(key) & 0x7FFFFFFFu;
+      } else {
+        if (blockIdx.x == 0 && slot < (uint32_t)max_slots) atomicOr(err, TRAIL_DEV_NONFIN);
+        kb = 0x7F800000u;
+      }
+      r.keybits = (forced ? 0u : 0x80000000u) | kb;
+      r.arrival = (uint32_t)in.key;
+      r.kv = (uint32_t)kvb;
+      r.gid = ((id_base + slot) & 0x7FFFFFFFu) | (run ? 0x80000000u : 0u);
+    }
     RkItem it;
     it.key = rk_key(r);
     const bool valid = it.key != ~0ull;
@@ -263,20 +267,25 @@ trail_select_rank_kernel(const Record *__restrict__ rec_in, Record *__restrict__
   __syncthreads();
   if (tr && tid == 0) tr[3] = ptx::gtimer();
 
-  // 3. per-CTA totals, then the last CTA writes the preempt list (positions need R(cut))
+  // 3. per-CTA totals in ONE 64-bit acq_rel atomic (done:16 | run-set size:24 | running in
+  //    the run set:24): the last CTA gets every total from the returned value
+  __shared__ unsigned long long s_tot;
   if (tid == 0) {
-    if (s_cta_run) atomicAdd(gcnt + 1, s_cta_run);
-    if (s_cta_rcut) atomicAdd(gcnt + 2, s_cta_rcut);
-    __threadfence();
-    const uint32_t old = atomicAdd(gcnt, 1u);
-    sh.last = old == gridDim.x - 1 ? 1 : 0;
+    const unsigned long long inc = (1ull << 48) | ((unsigned long long)s_cta_run << 24) |
+                                   (unsigned long long)s_cta_rcut;
+    unsigned long long old;
+    asm volatile("atom.add.acq_rel.gpu.u64 %0, [%1], %2;"
+                 : "=l"(old) : "l"(gcnt), "l"(inc) : "memory");
+    const unsigned long long tot = old + inc;
+    sh.last = (int)(tot >> 48) == (int)gridDim.x ? 1 : 0;
+    if (sh.last) *reinterpret_cast<unsigned long long *>(gcnt) = 0ull;   // re-arm
+    s_tot = tot;
   }
   __syncthreads();
   if (tr && tid == 0) { tr[4] = ptx::gtimer(); tr[14] = sh.last; }
   if (!sh.last) return;
-  __threadfence();
-  const int n_run = (int)__ldcg(gcnt + 1);
-  const int R_cut = (int)__ldcg(gcnt + 2);
+  const int n_run = (int)((s_tot >> 24) & 0xFFFFFFull);
+  const int R_cut = (int)(s_tot & 0xFFFFFFull);
   if (tr && tid == 0) tr[5] = ptx::gtimer();
   for (int p = n_run + tid; p < nv; p += kT) {
     const uint2 v = __ldcg(scratch + p);
@@ -289,7 +298,6 @@ trail_select_rank_kernel(const Record *__restrict__ rec_in, Record *__restrict__
     counts[1] = R_total - R_cut;
     counts[2] = n_run - R_cut;
     counts[3] = over ? TRAIL_WARN_OVER_BUDGET : TRAIL_OK;
-    gcnt[0] = 0u; gcnt[1] = 0u; gcnt[2] = 0u;      // re-arm for the next launch
   }
   if (tr && tid == 0) tr[7] = ptx::gtimer();
   (void)lane;
