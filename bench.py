@@ -46,6 +46,7 @@ CONFIGS = {
     "c1": dict(n=64, waiting=16, d=4096, H=512, k=10, dtype="f32", c=0.8, total=512.0,
                desc="64 running requests, d=4096, MLP 4096->512->10, fp32"),
     "c4": dict(n=16384, waiting=4096, d=8192, H=512, k=20, dtype="bf16", c=0.8, total=1024.0,
+               burst=False, distinct=4,
                desc="16384 requests/GPU at d=8192 (70B-shaped), 20 bins, tcgen05 GEMM regime"),
 }
 
@@ -124,8 +125,11 @@ def make_batches(cfg, nb: int, rank: int, world: int, seed: int):
     """The scripted engine (open loop): an initial burst prefill (P:570 shape: every
     request pools its prompt) that initialises the slots, then nb consecutive steady-state
     iterations (decode + the Alpaca-like trickle of completions/arrivals) that are timed."""
+    # configs whose burst prefill would not fit host memory (c4: 16K prompts x 8K wide) start
+    # from staggered decode ages instead (slots are first observed by their decode row, D-23)
     eng = W.EngineScript(cfg["n"], cfg["waiting"], d=cfg["d"], dtype=cfg["dtype"],
-                         seed=seed + 1000 * rank, arrival_base=rank, arrival_stride=world)
+                         seed=seed + 1000 * rank, arrival_base=rank, arrival_stride=world,
+                         burst_start=cfg.get("burst", True))
     init = eng.batch()
     eng.advance()
     batches = []
@@ -164,7 +168,7 @@ def run_ours(args, cfg):
     load_library()
     hbm, tf_burst, tf_sust, peak_src = peaks()
 
-    nb = max(1, min(args.distinct, args.steps + args.warmup))
+    nb = max(1, min(args.distinct, cfg.get("distinct", args.distinct), args.steps + args.warmup))
     eng, init, batches = make_batches(cfg, nb, rank, world, args.seed)
     w = W.make_weights(cfg["d"], cfg["H"], cfg["k"], cfg["dtype"],
                        edges=W.paper_bin_edges(cfg["k"], cfg["total"]), seed=args.seed)
@@ -319,7 +323,7 @@ def run_ours(args, cfg):
     # ---- burst prefill (P:570 shape): every request mean-pools its prompt rows (K1 streams
     # ~(rows + n) * d * eb bytes); reported beside the steady-state step, not in `value`
     burst = None
-    if not args.no_burst:
+    if not args.no_burst and cfg.get("burst", True):
         bt = []
         trail_profile_enable(t.h, 2)
         for _ in range(5):
@@ -484,7 +488,7 @@ def _threads():
 
 def oracle_steps(cfg, args, seconds: float, max_steps: int):
     from oracle import trail_ref as R
-    nb = max(1, min(args.distinct, max_steps))
+    nb = max(1, min(args.distinct, cfg.get("distinct", args.distinct), max_steps))
     eng, init, batches = make_batches(cfg, nb, 0, 1, args.seed)
     w = W.make_weights(cfg["d"], cfg["H"], cfg["k"], cfg["dtype"],
                        edges=W.paper_bin_edges(cfg["k"], cfg["total"]), seed=args.seed)
@@ -492,14 +496,21 @@ def oracle_steps(cfg, args, seconds: float, max_steps: int):
                       cfg["c"], eng.max_slots, x_dtype=cfg["dtype"])
     o.predict_step(W.decode(init.emb, cfg["dtype"]), init.row_offsets, init.request_ids,
                    init.is_prefill)                      # burst prefill, untimed
-    emb64 = [W.decode(b.emb, cfg["dtype"]) for b in batches]
+    cache = {}
+
+    def emb64(i):   # decoded lazily (c4: 1 GB of fp64 per batch)
+        if i not in cache:
+            if len(cache) >= 2:
+                cache.pop(next(iter(cache)))
+            cache[i] = W.decode(batches[i].emb, cfg["dtype"])
+        return cache[i]
     times, reqs = [], 0
     t_start = time.perf_counter()
     for s in range(max_steps):
         i = s % nb
         b = batches[i]
         t0 = time.perf_counter()
-        o.predict_step(emb64[i], b.row_offsets, b.request_ids, b.is_prefill)
+        o.predict_step(emb64(i), b.row_offsets, b.request_ids, b.is_prefill)
         o.schedule_step(b.sched_ids, b.arrival_seq, b.kv_blocks, b.is_running, b.kv_budget)
         times.append(time.perf_counter() - t0)
         reqs += b.n
