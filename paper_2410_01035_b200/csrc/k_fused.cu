@@ -190,7 +190,7 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
                            const float *__restrict__ prior_override, int max_slots,
                            float *__restrict__ lq_state, SlotMeta *__restrict__ meta,
                            float *__restrict__ post, float *__restrict__ Lout,
-                           uint32_t *__restrict__ err, uint64_t *__restrict__ trace) {
+                           uint32_t *__restrict__ err, uint64_t *__restrict__ trace, int spin) {
   using C = FCfg<KB>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -491,17 +491,28 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
   }
   if (tr && tid == 0) tr[7] = gtimer();
 
-  // ---- 4. last column tile of this row group runs the head
+  // ---- 4. head (row a3) once the NT column tiles of this row group have their z_part.
+  //    spin mode (the whole grid is one wave, so the NT CTAs are co-resident): every column
+  //    tile waits for the group's epoch counter and runs the head for rows r = nt (mod NT);
+  //    otherwise the last CTA to arrive runs the head for all rows of the group.
   __syncthreads();
   if (tid == 0) {
     uint32_t *cnt = arrive_cnt + (int64_t)blockIdx.x * MAXS + crank;
     uint32_t old;
-    // release: this CTA's z_part stores (ordered before by the barrier); acquire: the other
-    // column tiles' stores, for the head
+    // release: this CTA's z_part stores (ordered before it by the barrier)
     asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
-    const bool last = old == (uint32_t)(NT - 1);
-    if (last) *cnt = 0u;                        // re-arm for the next launch
-    *flag = last ? 1u : 0u;
+    if (spin) {
+      const uint32_t target = (old / (uint32_t)NT + 1u) * (uint32_t)NT;   // monotone epochs
+      uint32_t cur = old + 1u;
+      while ((int)(cur - target) < 0) {
+        __nanosleep(32);
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(cnt) : "memory");
+      }
+      *flag = 1u;
+    } else {
+      const bool last = old % (uint32_t)NT == (uint32_t)(NT - 1);
+      *flag = last ? 1u : 0u;
+    }
   }
   __syncthreads();
   if (tr && tid == 0) tr[9] = gtimer();
@@ -509,17 +520,21 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
     // one lane per bin, SEG-lane segments (2 requests per warp for k <= 16)
     const int SEG = k <= 16 ? 16 : 32;
     const int per_warp = 32 / SEG, seg = lane / SEG, b = lane % SEG;
+    const int rstep = spin ? NT : 1, rfirst = spin ? nt : 0;
+    const int my_rows = rows > rfirst ? (rows - rfirst + rstep - 1) / rstep : 0;
     const HeadSmem &hc = *reinterpret_cast<const HeadSmem *>(smem + C::HC_OFF);
-    for (int base = warp * per_warp; base < rows; base += (THREADS / 32) * per_warp) {
-      const int r = base + seg;
-      const int j = r < rows ? m0 + r0 + r : n;
+    for (int base = warp * per_warp; base < my_rows; base += (THREADS / 32) * per_warp) {
+      const int q = base + seg;
+      const int r = rfirst + q * rstep;
+      const bool rv = q < my_rows;
+      const int j = rv ? m0 + r0 + r : n;
       float z = 0.f;
       if (j < n && b < k) {
         z = __ldg(b2 + b);
         for (int t = 0; t < NT; ++t) z += __ldcg(zpart + ((int64_t)j * NT + t) * k + b);
       }
-      const int rr = r < rows ? r : 0;
-      head_seg(j, n, k, SEG, b, z, hc, r < rows ? s_slot[r] : 0xFFFFFFFFu, s_meta[rr],
+      const int rr = rv ? r : 0;
+      head_seg(j, n, k, SEG, b, z, hc, rv ? s_slot[r] : 0xFFFFFFFFu, s_meta[rr],
                b < KB ? s_lq[rr * KB + (b < KB ? b : 0)] : -INFINITY, prior_override, lq_state,
                meta, post, Lout, err);
     }
@@ -636,6 +651,9 @@ cudaError_t launch_fused_predict(Ctx &c, const void *emb, int64_t ld, const int3
   uint64_t *trace =
       (c.trace && (int)(cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z) <= c.trace_cap) ? c.trace
                                                                                        : nullptr;
+  // the spin-wait head needs every cluster resident at once (one wave)
+  const int tiles = (int)(cfg.gridDim.x * cfg.gridDim.y);
+  const int spin = (splits <= MAXS && tiles <= c.fused_max_clusters[splits] && !getenv("TRAIL_HEAD_LAST")) ? 1 : 0;
 #define TRAIL_FUSED(KB)                                                                          \
   cfg.dynamicSmemBytes = FCfg<KB>::SMEM_TOTAL;                                                     \
   return cudaLaunchKernelEx(&cfg, trail_fused_predict_kernel<KB>, c.tmap_emb, c.tmap_emb4,       \
@@ -644,7 +662,7 @@ cudaError_t launch_fused_predict(Ctx &c, const void *emb, int64_t ld, const int3
                             c.d / BK, splits, (const float *)c.b1, (const float *)c.w2,           \
                             (const float *)c.b2, c.host_consts, c.zpart,                                  \
                             c.arrive_cnt, ids, is_prefill, prior_override, c.cfg.max_slots, c.lq, \
-                            c.meta, post, L, c.dev_err, trace)
+                            c.meta, post, L, c.dev_err, trace, spin)
   switch (fused_kb(c.k)) {
     case 10: TRAIL_FUSED(10);
     case 16: TRAIL_FUSED(16);
