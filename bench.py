@@ -314,9 +314,16 @@ def run_ours(args, cfg):
         byts = 16.0 * float(np.mean([x["m"] for x in dev])) * world * 3
         ach = byts / (avg[dom] / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp) and args.config == "c2" and world == 1:
+        with open(tp) as f:
+            traffic = json.load(f).get(dom)
     if roof is not None:
         roof.update({"kernel": dom, "peak_source": peak_src, "avg_launch_us": avg[dom] * 1e3,
-                     "traffic": None,
+                     "traffic": traffic,
+                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram bytes "
+                                       "per launch)" if traffic else None,
                      "kernel_us": {k: round(v * 1e3, 3) for k, v in avg.items()},
                      "share_of_step": avg[dom] / ms_per_step})
 
@@ -350,7 +357,9 @@ def run_ours(args, cfg):
     e2e = run_e2e(args, cfg, t, batches, stream, flush, torch, device, world)
 
     # ---- gpu launches of our kernels in the timed region
-    per_step = 5  # pool, layer-1 (GEMV or tcgen05), head, pack, select
+    # our kernels per step: pool + fused tcgen05 (or pool + GEMV + head) + select (+ pack when
+    # the records are all-gathered)
+    per_step = (2 if mode == 2 else 3) + (2 if world > 1 else 1)
     gpu_launches = per_step * args.steps
 
     out = None
