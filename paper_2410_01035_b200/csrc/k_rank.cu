@@ -119,7 +119,7 @@ trail_select_rank_kernel(const Record *__restrict__ rec_in, Record *__restrict__
   __shared__ unsigned long long s_part[kT / 32][3];
   __shared__ uint32_t s_cta_run, s_cta_rcut;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint64_t *tr = trace ? trace + 16 * (int64_t)blockIdx.x : nullptr;   // diagnostics
+  uint64_t *tr = trace ? trace + 16 * (2048 + (int64_t)blockIdx.x) : nullptr;   // diagnostics
   if (tr && tid == 0) tr[0] = ptx::gtimer();
   if (tid == 0) { s_cta_run = 0u; s_cta_rcut = 0u; }
   // inputs of the local path are the caller's (not produced by the predict kernels): stage
@@ -307,8 +307,12 @@ trail_select_rank_kernel(const Record *__restrict__ rec_in, Record *__restrict__
 int select_rank_capacity() { return kRankCap; }
 
 cudaError_t select_rank_prepare() {
-  return cudaFuncSetAttribute(trail_select_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              kRankCap * (int)sizeof(RkItem));
+  cudaError_t e = cudaFuncSetAttribute(trail_select_rank_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kRankCap * (int)sizeof(RkItem));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(trail_select_rank_kernel,
+                              cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
 cudaError_t launch_select_rank(const Ctx &c, const Record *rec_in, Record *rec_out,
@@ -329,7 +333,7 @@ cudaError_t launch_select_rank(const Ctx &c, const Record *rec_in, Record *rec_o
                   c.cfg.max_slots, c.cfg.id_base, c.dev_err, n, ipc_log2, (long long)budget,
                   max_run, reinterpret_cast<uint2 *>(c.rank_sorted), c.rank_cnt, run, pre, adm,
                   counts,
-                  (c.trace && grid <= c.trace_cap && getenv("TRAIL_TRACE_SELECT")) ? c.trace
+                  (c.trace && 2048 + grid <= c.trace_cap) ? c.trace
                                                                                    : nullptr);
 }
 

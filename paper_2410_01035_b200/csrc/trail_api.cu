@@ -314,6 +314,7 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
       cudaMemset(c.xs, 0, (size_t)g.max_requests * c.d * c.esize) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
   if (umma_prepare(c) != cudaSuccess || head_prepare(c) != cudaSuccess ||
+      pool_prepare() != cudaSuccess ||
       fused_prepare(c) != cudaSuccess || select_prepare(c) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(TRAIL_ERR_CUDA);

@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-timeout 300 python scripts/trace_fused.py --n 512 --splits 0 > gpurun_out/trace_f.log 2>&1
-cat gpurun_out/trace_f.log
+TRAIL_FUSED_SPLITS=1 timeout 300 python scripts/trace_step.py 512 2>&1 | tail -1
+TRAIL_FUSED_SPLITS=2 timeout 300 python scripts/trace_step.py 512 2>&1 | tail -1
+TRAIL_PDL=0 timeout 300 python scripts/trace_step.py 512 2>&1 | tail -1
