@@ -71,10 +71,9 @@ cudaError_t launch_pack(const Ctx &c, const uint32_t *ids, const uint32_t *arriv
                         const int32_t *kv, const uint8_t *running, int n, Record *out,
                         int n_pad_to, cudaStream_t s) {
   if (n_pad_to <= 0) return cudaSuccess;
-  trail_pack_kernel<<<(n_pad_to + 255) / 256, 256, 0, s>>>(ids, arrival, kv, running, c.meta,
-                                                          c.consts, n, n_pad_to, c.cfg.max_slots,
-                                                          c.cfg.id_base, out, c.dev_err);
-  return cudaGetLastError();
+  return launch_k(trail_pack_kernel, dim3((n_pad_to + 255) / 256), dim3(256), 0, s, ids, arrival,
+                  kv, running, (const SlotMeta *)c.meta, (const HeadConsts *)c.consts, n, n_pad_to,
+                  c.cfg.max_slots, c.cfg.id_base, out, c.dev_err);
 }
 
 // ------------------------------------------------------------------ K4 select
@@ -273,6 +272,7 @@ cudaError_t select_prepare(Ctx &c) {
   cudaError_t e = select_fast_prepare();
   if (e == cudaSuccess) e = select_radix_prepare();
   if (e == cudaSuccess) e = select_rank_prepare();
+  if (e == cudaSuccess) e = select_bucket_prepare();
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(trail_select_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               kSmemCapRecords * 12);
@@ -281,9 +281,11 @@ cudaError_t select_prepare(Ctx &c) {
 cudaError_t launch_select(const Ctx &c, const Record *rec, int n, int64_t budget, int max_run,
                           uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
                           cudaStream_t s) {
-  if (select_impl() == 0 && n <= select_rank_capacity())
+  if (select_impl() == 0 && n <= kRankMaxRecords)
     return launch_select_rank(c, rec, nullptr, nullptr, nullptr, nullptr, nullptr, n, budget,
                               max_run, run, pre, adm, counts, s);
+  if (select_impl() == 0 && n <= c.bk_cap)
+    return launch_select_bucket(c, rec, n, budget, max_run, run, pre, adm, counts, s);
   if (select_impl() != 2 && n <= select_radix_capacity())
     return launch_select_radix(c, rec, nullptr, nullptr, nullptr, nullptr, nullptr, n, budget,
                                max_run, run, pre, adm, counts, s);

@@ -133,7 +133,7 @@ trail_status set_device(const Ctx &c) {
 void free_ctx(Ctx &c) {
   void *ptrs[] = {c.w1, c.b1, c.w2, c.b2, c.consts, c.lq, c.meta, c.dev_err, c.xs,
                   c.partial, c.rec_local, c.rec_all, c.sel_scratch, c.zpart, c.arrive_cnt, c.trace,
-                  c.rank_sorted, c.rank_cnt, c.pool_head, c.pool_tail, c.pool_cnt};
+                  c.rank_sorted, c.rank_cnt, c.pool_head, c.pool_tail, c.pool_cnt, c.bk_ws};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c.prof_ev) {
@@ -291,6 +291,10 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
   if (cudaMemset(c.pool_cnt, 0, (size_t)g.max_requests * sizeof(uint32_t)) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
   ALLOC(c.rank_sorted, (size_t)max_sched * c.world * sizeof(Record));
+  c.bk_cap = max_sched * c.world;
+  ALLOC(c.bk_ws, bucket_workspace_bytes(c.bk_cap));
+  if (cudaMemset(c.bk_ws, 0, bucket_workspace_bytes(c.bk_cap)) != cudaSuccess)
+    return fail(TRAIL_ERR_CUDA);
   ALLOC(c.rank_cnt, 16 * sizeof(uint32_t));
   if (cudaMemset(c.rank_cnt, 0, 16 * sizeof(uint32_t)) != cudaSuccess) return fail(TRAIL_ERR_CUDA);
   c.sel_scratch_bytes = select_scratch_bytes(max_sched * c.world);
@@ -652,7 +656,7 @@ int select_impl() {
 bool use_bitonic_select() { return select_impl() == 2; }
 int select_local_capacity() {
   switch (select_impl()) {
-    case 0: return select_rank_capacity();
+    case 0: return kRankMaxRecords;
     case 1: return select_radix_capacity();
     default: return select_fast_capacity();
   }

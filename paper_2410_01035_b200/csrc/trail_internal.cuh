@@ -69,6 +69,8 @@ struct Ctx {
   float *pool_head = nullptr;       // [pool_grid][d] K1 partial sums (request began earlier)
   float *pool_tail = nullptr;       // [pool_grid][d] K1 partial sums (request continues)
   uint32_t *pool_cnt = nullptr;     // [max_requests] K1 per-request chunk arrival counters
+  void *bk_ws = nullptr;            // bucketed selection workspace (k_bucket.cu)
+  int bk_cap = 0;                   // records it holds
   Record *rank_sorted = nullptr;    // [max_sched * world] rank-select scatter target
   uint32_t *rank_cnt = nullptr;     // rank-select CTA completion counter  // fused kernel: resident clusters of size s (occupancy)
   Record *rec_local = nullptr; // [max_sched]
@@ -149,6 +151,12 @@ cudaError_t launch_select_local(const Ctx &c, const uint32_t *ids, const uint32_
                                 int max_run, uint32_t *run, uint32_t *pre, uint32_t *adm,
                                 int32_t *counts, cudaStream_t s);
 cudaError_t select_rank_prepare();
+cudaError_t select_bucket_prepare();
+size_t bucket_workspace_bytes(int m_max);
+cudaError_t launch_select_bucket(const Ctx &c, const Record *rec, int m, int64_t budget,
+                                 int max_run, uint32_t *run, uint32_t *pre, uint32_t *adm,
+                                 int32_t *counts, cudaStream_t s);
+constexpr int kRankMaxRecords = 2048;   // rank-counting kernel below, bucketed kernels above
 int select_rank_capacity();
 cudaError_t launch_select_rank(const Ctx &c, const Record *rec_in, Record *rec_out,
                                const uint32_t *ids, const uint32_t *arrival, const int32_t *kv,
