@@ -221,6 +221,13 @@ TRAIL_API trail_status trail_trace_read(trail_handle h, uint64_t *host_out, int3
 /* Overrides cfg.l1_mode for subsequent calls (the tcgen05 modes require bf16). */
 TRAIL_API trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode);
 
+/* Optional host-side hint: the number of embedding rows (the flat batch's token count,
+ * row_offsets[n] - row_offsets[0]) of the next trail_predict_step calls; 0 = unknown (the
+ * default).  It only selects the pooling kernel variant (bulk-copy streaming for
+ * prefill-heavy batches, P:570 burst shape); results are bit-identical either way.  Kept
+ * until changed.  Errors: TRAIL_ERR_INVALID (rows < 0). */
+TRAIL_API trail_status trail_set_rows_hint(trail_handle h, int64_t rows);
+
 /* Which layer-1 kernel trail_predict_step uses for n requests, and its split-K factor. */
 TRAIL_API trail_status trail_plan_l1(trail_handle h, int32_t n, int32_t *l1_mode_out,
                            int32_t *splits_out);

@@ -371,6 +371,12 @@ trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode) {
   return TRAIL_OK;
 }
 
+trail_status trail_set_rows_hint(trail_handle h, int64_t rows) {
+  if (!h || rows < 0) return TRAIL_ERR_INVALID;
+  h->c.rows_hint = rows;
+  return TRAIL_OK;
+}
+
 trail_status trail_plan_l1(trail_handle h, int32_t n, int32_t *l1_mode_out, int32_t *splits_out) {
   if (!h || n < 0) return TRAIL_ERR_INVALID;
   int mode, bn, s;

@@ -86,6 +86,7 @@ struct Ctx {
   int64_t tmap_emb_ld = 0;
   bool have_tmaps = false;
   int num_sms = 148;
+  int64_t rows_hint = 0;        // trail_set_rows_hint: embedding rows of the next predict steps
   // NCCL
   void *nccl_comm = nullptr;
   int rank = 0, world = 1;
@@ -110,6 +111,7 @@ struct Ctx {
 cudaError_t launch_pool(const Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
                         int write_singles, cudaStream_t s);
 int pool_grid(const Ctx &c);
+bool pool_use_bulk();
 cudaError_t pool_prepare();
 cudaError_t launch_gemv_l1(const Ctx &c, int n, int splits, cudaStream_t s);
 cudaError_t launch_umma_l1(const Ctx &c, int n, int bn, int splits, cudaStream_t s);

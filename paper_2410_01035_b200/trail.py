@@ -79,6 +79,7 @@ _SIGS = {
     "trail_profile_read": ([_P, _I32, ctypes.POINTER(ctypes.c_double),
                             ctypes.POINTER(ctypes.c_int64), _I32], _I32),
     "trail_set_l1_mode": ([_P, _I32], _I32),
+    "trail_set_rows_hint": ([_P, _I64], _I32),
     "trail_trace_enable": ([_P, _I32], _I32),
     "trail_trace_read": ([_P, _P, _I32], _I32),
     "trail_plan_l1": ([_P, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)], _I32),
@@ -236,6 +237,10 @@ def trail_set_l1_mode(h, mode: int) -> None:
     _check("trail_set_l1_mode", _lib().trail_set_l1_mode(h, int(mode)))
 
 
+def trail_set_rows_hint(h, rows: int) -> None:
+    _check("trail_set_rows_hint", _lib().trail_set_rows_hint(h, int(rows)))
+
+
 def trail_plan_l1(h, n: int):
     mode, splits = _I32(0), _I32(0)
     _check("trail_plan_l1", _lib().trail_plan_l1(h, int(n), ctypes.byref(mode), ctypes.byref(splits)))
@@ -298,8 +303,13 @@ class Trail:
             pass
 
     def predict(self, emb, row_offsets, request_ids, is_prefill, prior_override=None,
-                stream=None):
+                stream=None, rows=None):
         n = int(request_ids.shape[0])
+        # host-side row count of the flat batch (selects the pooling kernel variant only)
+        rows = int(emb.shape[0]) if rows is None and emb.dim() == 2 else int(rows or 0)
+        if rows != getattr(self, "_rows_hint", 0):
+            trail_set_rows_hint(self.h, rows)
+            self._rows_hint = rows
         trail_predict_step(self.h, emb, emb.shape[1] if emb.dim() == 2 else self.d, row_offsets,
                            request_ids, is_prefill, prior_override, n, self.post, self.L, stream)
         return self.post[:n], self.L[:n]

@@ -1,0 +1,133 @@
+// HBM read-streaming ceiling on the B200 box (diagnostic, not product code): how fast can a
+// kernel read a large contiguous buffer with (a) 16-byte register loads, U in flight per
+// thread, and (b) 1-D bulk copies into a shared-memory ring?  Flush before each run by
+// writing (dirty L2) or reading (clean L2) a 256 MiB buffer.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 stream.cu -o stream && ./stream
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int U>
+__global__ void read_reg(const uint4 *__restrict__ p, int64_t nvec, uint32_t *out) {
+  const int64_t per = (nvec + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * per, hi = min(nvec, lo + per);
+  uint32_t acc = 0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += (int64_t)U * blockDim.x) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = i + (int64_t)u * blockDim.x;
+      v[u] = k < hi ? __ldg(p + k) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+  }
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
+__device__ __forceinline__ void wait_bar(uint32_t bar, uint32_t ph) {
+  uint32_t ok = 0;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+                 : "=r"(ok) : "r"(bar), "r"(ph) : "memory");
+  } while (!ok);
+}
+
+// ring of NS stages of SB bytes, one bulk copy per stage, thread 0 produces
+__global__ void read_bulk(const uint8_t *__restrict__ p, int64_t bytes, int NS, int SB, uint32_t *out) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(sm);
+  const uint32_t full = ring + NS * SB, empty = full + 8 * NS;
+  const int64_t per = ((bytes / gridDim.x) + SB - 1) / SB * SB;
+  const int64_t lo = blockIdx.x * per, hi = min(bytes, lo + per);
+  const int nst = hi > lo ? (int)((hi - lo + SB - 1) / SB) : 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full + 8 * i));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty + 8 * i), "r"(blockDim.x / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int st) {
+    const int b = st % NS;
+    const int64_t o = lo + (int64_t)st * SB;
+    const uint32_t sz = (uint32_t)min((int64_t)SB, hi - o);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full + 8 * b), "r"(sz) : "memory");
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(ring + b * SB), "l"(p + o), "r"(sz), "r"(full + 8 * b) : "memory");
+  };
+  if (threadIdx.x == 0)
+    for (int s = 0; s < min(nst, NS); ++s) issue(s);
+  uint32_t acc = 0;
+  for (int st = 0; st < nst; ++st) {
+    const int b = st % NS;
+    if (threadIdx.x == 0 && st >= 1 && st - 1 + NS < nst) {
+      wait_bar(empty + 8 * ((st - 1) % NS), ((st - 1) / NS) & 1);
+      issue(st - 1 + NS);
+    }
+    wait_bar(full + 8 * b, (st / NS) & 1);
+    const uint4 *s = reinterpret_cast<const uint4 *>(sm + b * SB);
+    const int nv = (int)(min((int64_t)SB, hi - (lo + (int64_t)st * SB)) / 16);
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) { uint4 v = s[i]; acc ^= v.x ^ v.y ^ v.z ^ v.w; }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty + 8 * b) : "memory");
+  }
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int64_t bytes = 162LL << 20, fb = 256LL << 20;
+  uint8_t *buf, *flush;
+  uint32_t *out;
+  cudaMalloc(&buf, bytes);
+  cudaMalloc(&flush, fb);
+  cudaMalloc(&out, 4);
+  cudaMemset(buf, 1, bytes);
+  cudaFuncSetAttribute(read_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto run = [&](const char *name, auto launch) {
+    for (int dirty = 1; dirty >= 0; --dirty) {
+      float best = 1e9f, sum = 0.f;
+      for (int it = 0; it < 7; ++it) {
+        if (dirty) cudaMemsetAsync(flush, it, fb);
+        else read_reg<8><<<sms * 2, 512>>>((const uint4 *)flush, fb / 16, out);
+        cudaEventRecord(a);
+        launch();
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (it >= 2) { best = ms < best ? ms : best; sum += ms; }
+      }
+      printf("%-34s %s  best %7.2f us  %7.1f GB/s   mean %7.1f GB/s\n", name, dirty ? "dirty" : "clean",
+             best * 1e3, bytes / (best * 1e-3) / 1e9, bytes / (sum / 5 * 1e-3) / 1e9);
+    }
+  };
+  char nm[64];
+  for (int g : {1, 2})
+    for (int t : {256, 512, 1024}) {
+      snprintf(nm, 64, "reg U=8  G=%dxSM T=%d", g, t);
+      run(nm, [&] { read_reg<8><<<sms * g, t>>>((const uint4 *)buf, bytes / 16, out); });
+    }
+  for (int t : {256, 512}) {
+    snprintf(nm, 64, "reg U=16 G=1xSM T=%d", t);
+    run(nm, [&] { read_reg<16><<<sms, t>>>((const uint4 *)buf, bytes / 16, out); });
+  }
+  for (int ns : {4, 6, 12})
+    for (int sb : {16384, 32768}) {
+      if (ns * sb > 200 * 1024) continue;
+      snprintf(nm, 64, "bulk NS=%d SB=%dK T=256", ns, sb / 1024);
+      run(nm, [&] { read_bulk<<<sms, 256, ns * sb + 16 * ns>>>(buf, bytes, ns, sb, out); });
+    }
+  run("bulk NS=3 SB=64K T=256", [&] { read_bulk<<<sms, 256, 3 * 65536 + 16 * 3>>>(buf, bytes, 3, 65536, out); });
+  run("bulk NS=4 SB=48K T=256", [&] { read_bulk<<<sms, 256, 4 * 49152 + 16 * 4>>>(buf, bytes, 4, 49152, out); });
+  run("bulk NS=24 SB=8K T=256", [&] { read_bulk<<<sms, 256, 24 * 8192 + 16 * 24>>>(buf, bytes, 24, 8192, out); });
+  run("cudaMemcpy D2D (r+w bytes/2)", [&] { cudaMemcpyAsync(flush, buf, bytes, cudaMemcpyDeviceToDevice); });
+  printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}

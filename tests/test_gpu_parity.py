@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 from oracle import trail_ref as R  # noqa: E402
 from synth import workload as W  # noqa: E402
 
-from gpu_util import (assert_predict_close, gpu_keys_forced, gpu_predict, gpu_schedule,  # noqa: E402
+from gpu_util import (assert_predict_close, dev, gpu_keys_forced, gpu_predict, gpu_schedule,  # noqa: E402
                       gpu_state, make_pair, oracle_predict, top2_gap)
 
 
@@ -103,6 +103,38 @@ def test_prefill_pooling_long_prompts_and_outliers():
     qg, Lg = gpu_predict(t, emb, off, ids[:4], pref)
     qo, Lo = oracle_predict(o, emb, off, ids[:4], pref, "bf16")
     assert_predict_close(qg, Lg, qo, Lo)
+
+
+@pytest.mark.parametrize("dtype,n,d,pad,pf", [
+    ("bf16", 512, 4096, 0, 1.0),      # burst prefill (P:570 shape), config 2 width
+    ("bf16", 300, 4096, 64, 0.7),     # row stride > d, decode rows mixed in
+    ("bf16", 160, 8192, 0, 1.0),      # config 4 width: 2 rows per 32 KB stage
+    ("f32", 128, 4096, 32, 1.0),      # config 1 dtype
+])
+def test_bulk_pool_bit_identical_to_register_pool(dtype, n, d, pad, pf):
+    """K1 bulk-copy variant (selected by the host row-count hint) against the register
+    variant (hint 0) and the oracle: same chunking and add order, so bit-identical."""
+    from paper_2410_01035_b200.trail import trail_predict_step, trail_set_rows_hint
+    H, k = 512, 20 if d == 8192 else 10
+    w = W.make_weights(d, H, k, dtype, seed=21)
+    emb, off, pref = W.make_step_inputs(n, d, dtype, prefill_frac=pf, seed=22)
+    rows = int(off[-1])
+    assert rows >= 8 * torch.cuda.get_device_properties(0).multi_processor_count
+    st = np.zeros((rows, d + pad), dtype=emb.dtype)
+    st[:, :d] = emb
+    e, o_, i_, p_ = dev(st), dev(off), dev(np.arange(n, dtype=np.uint32)), dev(pref)
+    outs = []
+    for hint in (0, rows):
+        t, o = make_pair(w, 0.8, n, n, n, dtype)
+        trail_set_rows_hint(t.h, hint)
+        trail_predict_step(t.h, e, d + pad, o_, i_, p_, None, n, t.post, t.L)
+        torch.cuda.synchronize()
+        outs.append((t.post[:n].cpu().numpy().copy(), t.L[:n].cpu().numpy().copy()))
+        t.close()
+    assert outs[0][0].tobytes() == outs[1][0].tobytes()
+    assert outs[0][1].tobytes() == outs[1][1].tobytes()
+    qo, Lo = oracle_predict(o, emb, off, np.arange(n, dtype=np.uint32), pref, dtype)
+    assert_predict_close(outs[1][0].astype(np.float64), outs[1][1].astype(np.float64), qo, Lo)
 
 
 def test_prior_override_and_uniform_reduces_to_softmax():
