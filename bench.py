@@ -385,7 +385,7 @@ def run_ours(args, cfg):
                             ": " + cfg["desc"],
                 "n_per_gpu": cfg["n"], "waiting_per_gpu": cfg["waiting"], "d": cfg["d"],
                 "hidden": cfg["H"], "bins": cfg["k"], "c": cfg["c"],
-                "l1_kernel": {1: "gemv", 2: "tcgen05"}[mode], "l1_splits": splits,
+                "l1_kernel": {1: "gemv", 2: "tcgen05 split-K (K2c)", 3: "tcgen05 unfused", 4: "tcgen05 CTA pair (K2d)"}[mode], "l1_splits": splits,
                 "l2": "flushed between timed steps (256 MiB memset outside the step events)"
                       if not args.no_flush else "warm",
                 "cuda_graph": use_graph,

@@ -53,12 +53,16 @@ typedef enum { TRAIL_F32 = 0, TRAIL_BF16 = 1 } trail_dtype;
 
 /* Layer-1 kernel selection (row a2). */
 typedef enum {
-  TRAIL_L1_AUTO = 0,   /* GEMV for fp32 or small n, fused tcgen05 kernel otherwise */
+  TRAIL_L1_AUTO = 0,   /* GEMV for fp32 or small n, fused tcgen05 kernel (K2c) for moderate n,
+                          wide CTA-pair kernel (K2d) for large n */
   TRAIL_L1_GEMV = 1,   /* K2a: warp-per-output-slice split-K GEMV (CUDA cores) + head K3 */
   TRAIL_L1_UMMA = 2,   /* K2c: fused TMA + tcgen05/TMEM layer 1, cluster split-K reduction,
                           layer 2 and head in the epilogue (bf16 only) */
-  TRAIL_L1_UMMA_UNFUSED = 3  /* K2b + K3: tcgen05 layer 1 with split-K partials in global
+  TRAIL_L1_UMMA_UNFUSED = 3, /* K2b + K3: tcgen05 layer 1 with split-K partials in global
                                 memory, then the separate head kernel (bf16 only) */
+  TRAIL_L1_WIDE = 4    /* K2d: CTA-pair (cta_group::2) tcgen05 layer 1 over the whole hidden
+                          width (H = 512) in TMEM, layer 2 and head in the epilogue; AUTO picks
+                          it for large n (bf16, H = 512 only) */
 } trail_l1_mode;
 
 /* Sticky device-side error bits (trail_device_errors). */

@@ -32,6 +32,8 @@
 
 #include <algorithm>
 
+#include "head_dev.cuh"
+#include "xgather.cuh"
 #include "sm100_ptx.cuh"
 #include "trail_internal.cuh"
 
@@ -75,103 +77,6 @@ struct FCfg {
 
 __host__ __device__ __forceinline__ int row_lo(int r, int S) { return (r * BM) / S; }
 }  // namespace
-
-// Per-bin constants of the head, staged in shared memory (lane b reads entry b).
-struct HeadSmem {
-  float m[kMaxBins], log_stay[kMaxBins], log_move[kMaxBins], log_prior[kMaxBins];
-  uint32_t thr[kMaxBins];
-};
-
-__device__ __forceinline__ float seg_max(float v, int seg) {
-  for (int o = seg >> 1; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o, seg));
-  return v;
-}
-__device__ __forceinline__ float seg_sum(float v, int seg) {
-  for (int o = seg >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, seg);
-  return v;
-}
-
-// Row a3 head for request j, one lane per bin (b) in a SEG-lane segment; every lane of the
-// warp calls it (j >= n: inactive segment, shuffles only).  Log-domain recursion (D-22) with
-// fast-math exp/log (MUFU, ~2 ulp: errors ~1e-7, far inside the 2e-3 posterior bound).
-//   log p = z - logsumexp(z)                                   (softmax)
-//   prefill: log q = log pi + log p                            (D-9 threshold)
-//   decode:  log q = logaddexp(log T_bb + lq(b), log T_b,b+1 + lq(b+1)) + log p
-//   normalise; L = sum_b q(b) m_b
-// Five segment reductions: max z, sum exp, (max, argmax) of the unnormalised log q, sum exp,
-// sum q m.  The D-5 fallback (all-zero product) needs max log p = max z - lse: no reduction.
-__device__ __forceinline__ void head_seg(int j, int n, int k, int SEG, int b, float z,
-                                         const HeadSmem &hc, uint32_t sl, const SlotMeta &mt,
-                                         float lq_prev, const float *__restrict__ prior_override,
-                                         float *__restrict__ lq_state, SlotMeta *__restrict__ meta,
-                                         float *__restrict__ post, float *__restrict__ Lout,
-                                         uint32_t *__restrict__ err) {
-  const bool act = j < n && b < k;
-  const bool bad = sl == 0xFFFFFFFFu;
-  const uint32_t slot = sl & 0x7FFFFFFFu;
-  if (!act) z = -INFINITY;
-  const float zmax = seg_max(z, SEG);
-  const float lse = zmax + __logf(seg_sum(act ? __expf(z - zmax) : 0.f, SEG));
-  const float lp = act ? z - lse : -INFINITY;
-  const bool first = (sl >> 31) != 0u || !(mt.flags & 1u);
-  const float prev = (act && !first && !bad) ? lq_prev : -INFINITY;
-  float prev1 = __shfl_down_sync(0xffffffffu, prev, 1, SEG);
-  if (b + 1 >= k) prev1 = -INFINITY;
-  float lq = -INFINITY;
-  if (act) {
-    float lpr;
-    if (first) {
-      lpr = prior_override ? __logf(__ldg(prior_override + (int64_t)j * k + b)) : hc.log_prior[b];
-    } else {
-      // prior(b) = (1 - 1/w_b) q(b) + (1/w_{b+1}) q(b+1): T applied to the posterior (D-1, D-2)
-      const float stay = hc.log_stay[b] + prev, move = hc.log_move[b] + prev1;
-      const float mx = fmaxf(stay, move), mn = fminf(stay, move);
-      lpr = mx == -INFINITY ? -INFINITY : mx + __logf(1.f + __expf(mn - mx));
-    }
-    lq = lpr + lp;
-  }
-  // (max, argmax) of the unnormalised log q, lowest index on ties (argmax of q^(0), D-9)
-  float qmax = lq;
-  int bi = act ? b : 0x7FFFFFFF;
-  for (int o = SEG >> 1; o > 0; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, qmax, o, SEG);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o, SEG);
-    if (ov > qmax || (ov == qmax && oi < bi)) { qmax = ov; bi = oi; }
-  }
-  if (qmax == -INFINITY) {          // all-zero product: fall back to p (D-5)
-    lq = lp;
-    qmax = zmax - lse;
-    bi = 0;                         // (only reachable for a zero prior on every bin)
-  }
-  const float qs = seg_sum(act ? __expf(lq - qmax) : 0.f, SEG);   // every lane shuffles
-  lq = act ? lq - (qmax + __logf(qs)) : -INFINITY;
-  const float q = act ? __expf(lq) : 0.f;
-  const float L = seg_sum(act ? q * hc.m[b] : 0.f, SEG);
-  if (j >= n) return;
-  if (bad) {
-    if (b == 0) atomicOr(err, TRAIL_DEV_BAD_ID);
-    if (b < k && post) post[(int64_t)j * k + b] = NAN;
-    if (b == 0 && Lout) Lout[j] = NAN;
-    return;
-  }
-  if (b < k) {
-    lq_state[(int64_t)slot * k + b] = lq;
-    if (post) post[(int64_t)j * k + b] = q;
-  }
-  if (b == 0) {
-    SlotMeta o = mt;
-    if (first) {
-      o.thr = hc.thr[bi];
-      o.age = 0;
-      o.flags = 1u;
-    } else {
-      o.age += 1;
-    }
-    o.L = L;
-    meta[slot] = o;
-    if (Lout) Lout[j] = L;
-  }
-}
 
 template <int KB>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -265,42 +170,8 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
     // 4l..4l+3 of the tile: one TMA tile::gather4 per k-block when all four come from emb,
     // else four single-row loads.  Only xs rows depend on the previous kernel (PDL): decode
     // tiles never wait for the pool kernel.
-    int src[4];
-    unsigned emask = 0u;                       // bit q: row 4*lane+q comes from emb
-    bool any_xs = false;
-    {
-      const int j4 = m0 + 4 * lane;
-      int o[5];
-#pragma unroll
-      for (int q = 0; q < 5; ++q) o[q] = (j4 + q <= n) ? __ldg(off + j4 + q) : 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = j4 + q;
-        const bool single = j < n && o[q + 1] - o[q] == 1;
-        src[q] = single ? o[q] : j;            // emb row, or xs row (padding rows: xs, unused)
-        emask |= single ? 1u << q : 0u;
-        any_xs |= !single && j < n;
-      }
-    }
-    // load plan of my 4-row group: runs of consecutive source rows become one TMA box
-    // (32 rows per 8-lane block, else 4 rows), scattered single rows a gather4, mixed
-    // groups four 1-row loads
-    const bool g_emb = emask == 0xFu, g_xs = emask == 0u;
-    const bool g_contig = src[1] == src[0] + 1 && src[2] == src[0] + 2 && src[3] == src[0] + 3;
-    const int prev_src0 = __shfl_up_sync(0xffffffffu, src[0], 1);
-    const bool link = (lane & 7) == 0 || prev_src0 + 4 == src[0];
-    const unsigned blk = 0xFFu << (lane & 24);
-    const bool b_emb = (__ballot_sync(0xffffffffu, g_emb && g_contig && link) & blk) == blk;
-    const bool b_xs = (__ballot_sync(0xffffffffu, g_xs && g_contig && link) & blk) == blk;
-    // mode: 0 none (covered by the block op), 1 block emb32, 2 block xs32, 3 emb4, 4 xs4,
-    //       5 gather4 (emb), 6 four single rows
-    int mode;
-    if (b_emb || b_xs) mode = (lane & 7) == 0 ? (b_emb ? 1 : 2) : 0;
-    else if (g_contig && g_emb) mode = 3;
-    else if (g_contig && g_xs) mode = 4;
-    else if (g_emb) mode = 5;
-    else mode = 6;
-    const bool tile_xs = __any_sync(0xffffffffu, any_xs);
+    const XPlan xp = xplan_make(off, n, m0, lane);
+    const bool tile_xs = xp.tile_xs;
     const int pre = nkb < STAGES ? nkb : STAGES;
     if (lane == 0)
       for (int i = 0; i < pre; ++i) {
@@ -321,21 +192,8 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
         }
         __syncwarp();
       }
-      const uint32_t dst = sA0 + st * A_BYTES + (uint32_t)(lane * 4 * 128);
-      const uint32_t fb = full0 + 8 * st;
-      switch (mode) {
-        case 1: tma_load_2d(dst, &tmap_emb32, fb, kc, src[0]); break;
-        case 2: tma_load_2d(dst, &tmap_xs32, fb, kc, src[0]); break;
-        case 3: tma_load_2d(dst, &tmap_emb4, fb, kc, src[0]); break;
-        case 4: tma_load_2d(dst, &tmap_xs4, fb, kc, src[0]); break;
-        case 5: tma_gather4(dst, &tmap_emb, fb, kc, src[0], src[1], src[2], src[3]); break;
-        case 6:
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            tma_load_2d(dst + q * 128, ((emask >> q) & 1u) ? &tmap_emb : &tmap_xs, fb, kc, src[q]);
-          break;
-        default: break;
-      }
+      xplan_issue<false>(xp, lane, sA0 + st * A_BYTES, full0 + 8 * st, kc, &tmap_emb, &tmap_emb4,
+                         &tmap_emb32, &tmap_xs, &tmap_xs4, &tmap_xs32);
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -616,20 +474,26 @@ int fused_splits(const Ctx &c, int n) {
   return best;
 }
 
+// row-gather tensor maps over the caller's embeddings (boxes 64 x {1, 4, 32}, SW128),
+// re-encoded only when the pointer or the row stride changes
+bool ensure_emb_tmaps(Ctx &c, const void *emb, int64_t ld) {
+  if (emb == c.tmap_emb_ptr && ld == c.tmap_emb_ld) return true;
+  const uint64_t rows = 0x7FFFFFFF;     // rows are addressed through off[] only
+  if (!encode_rows_bf16(&c.tmap_emb, emb, (uint64_t)c.d, rows, (uint64_t)ld, BK, 1) ||
+      !encode_rows_bf16(&c.tmap_emb4, emb, (uint64_t)c.d, rows, (uint64_t)ld, BK, 4) ||
+      !encode_rows_bf16(&c.tmap_emb32, emb, (uint64_t)c.d, rows, (uint64_t)ld, BK, 32))
+    return false;
+  c.tmap_emb_ptr = emb;
+  c.tmap_emb_ld = ld;
+  return true;
+}
+
 cudaError_t launch_fused_predict(Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
                                  int splits, const uint32_t *ids,
                                  const uint8_t *is_prefill, const float *prior_override,
                                  float *post, float *L, cudaStream_t s) {
   if (!c.have_tmaps) return cudaErrorInvalidValue;
-  if (emb != c.tmap_emb_ptr || ld != c.tmap_emb_ld) {   // row-gather map over the caller's rows
-    const uint64_t rows = 0x7FFFFFFF;     // rows are addressed through off[] only
-    if (!encode_rows_bf16(&c.tmap_emb, emb, (uint64_t)c.d, rows, (uint64_t)ld, BK, 1) ||
-        !encode_rows_bf16(&c.tmap_emb4, emb, (uint64_t)c.d, rows, (uint64_t)ld, BK, 4) ||
-        !encode_rows_bf16(&c.tmap_emb32, emb, (uint64_t)c.d, rows, (uint64_t)ld, BK, 32))
-      return cudaErrorInvalidValue;
-    c.tmap_emb_ptr = emb;
-    c.tmap_emb_ld = ld;
-  }
+  if (!ensure_emb_tmaps(c, emb, ld)) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((n + BM - 1) / BM, c.H / BN, splits);
   cfg.blockDim = dim3(THREADS);

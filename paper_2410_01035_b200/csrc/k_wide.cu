@@ -1,0 +1,337 @@
+// K2d — the wide predict kernel for large batches (rows a2 + a3): layer 1 on a CTA PAIR
+// (tcgen05.mma.cta_group::2, M = 256) with the whole hidden width H = 512 in TMEM, so
+// every request's h, layer 2 and head stay inside its own CTA — no split-K, no cross-CTA
+// reduction, no arrival counters, any number of waves.
+//
+//   P:201  h = ReLU(W1 x + b1) (d -> 512), z = W2 h + b2 (512 -> k)
+//   P:204/P:219-226  softmax, Bayesian refinement (log domain, D-22), L_t   (head_dev.cuh)
+//
+// Why: at configs[3] (16 384 x 8192) the split-K kernel K2c runs 512 tiles of 128 x 128 in
+// four waves and reads X four times (once per column tile) — 363 µs, L2/HBM-bound.  Here the
+// pair p owns requests [256p, 256p + 256): CTA r of the pair loads its 128 rows of X and the
+// W1 rows {128r .. 128r+127} and {256 + 128r .. 256 + 128r + 127} (its halves of the two
+// N = 256 MMAs) — 48 KB per 64-wide K block — and the even CTA issues two M = 256, N = 256,
+// K = 16 MMAs per 16 columns of K for both.  X is read from HBM exactly once.
+//   warp 0        : TMA producer (X gather shared with K2c, xgather.cuh; W1 2 x 128 x 64)
+//                   — cta_group::2 loads completing on the LEADER's full barrier
+//   warp 1, even  : MMA issuer; tcgen05.commit multicast frees the stage in both CTAs
+//   warps 2-7     : stage b1, head constants and the slot state of the CTA's 128 rows
+//   all 8 warps   : epilogue — TMEM (lane = row) -> +b1, ReLU -> layer-2 partials over two
+//                   column halves (fixed order) -> head, one lane per bin (head_dev.cuh)
+#include <math.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "head_dev.cuh"
+#include "sm100_ptx.cuh"
+#include "trail_internal.cuh"
+#include "xgather.cuh"
+
+namespace trail {
+
+using namespace ptx;
+
+namespace {
+constexpr int WT = 256;
+constexpr int WBM = 128;                       // rows per CTA (256 per pair)
+constexpr int WBK = 64;
+constexpr int WH = 512;                        // hidden width held in TMEM (fp32 columns)
+constexpr int WA = WBM * WBK * 2;              // 16 KB: my 128 rows of X
+constexpr int WBH = 128 * WBK * 2;             // 16 KB: my 128 rows of one N half of W1
+constexpr int WSTAGE = WA + 2 * WBH;           // 48 KB per CTA per K block
+constexpr int WSTAGES = 4;
+
+template <int KB>
+struct WCfg {
+  static constexpr int KBP = (KB + 3) & ~3;    // layer-2 bins padded to float4
+  static constexpr int PIPE = WSTAGES * WSTAGE;
+  static constexpr int BAR_OFF = PIPE;         // full[4], empty[4], done, tmem slot
+  static constexpr int B1_OFF = BAR_OFF + 256;
+  static constexpr int SLOT_OFF = B1_OFF + WH * 4;
+  static constexpr int META_OFF = SLOT_OFF + WBM * 4;
+  static constexpr int LQ_OFF = META_OFF + WBM * 16;
+  static constexpr int HC_OFF = LQ_OFF + WBM * KB * 4;
+  static constexpr int SMEM_USED = HC_OFF + (int)sizeof(HeadSmem);
+  static constexpr int SMEM_TOTAL = SMEM_USED + 1024;
+  // after the mainloop the pipeline buffers hold W2^T [512][KBP] and z [2][128][KBP]
+  static constexpr int W2S_OFF = 0;
+  static constexpr int ZS_OFF = WH * KBP * 4;
+  static_assert(ZS_OFF + 2 * WBM * KBP * 4 <= PIPE, "epilogue staging must fit the pipeline");
+  static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
+};
+}  // namespace
+
+template <int KB>
+__global__ void __launch_bounds__(WT, 1)
+trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
+                          const __grid_constant__ CUtensorMap tmap_emb4,
+                          const __grid_constant__ CUtensorMap tmap_emb32,
+                          const __grid_constant__ CUtensorMap tmap_xs,
+                          const __grid_constant__ CUtensorMap tmap_xs4,
+                          const __grid_constant__ CUtensorMap tmap_xs32,
+                          const __grid_constant__ CUtensorMap tmap_w,
+                          const int32_t *__restrict__ off, int n, int kblocks,
+                          const float *__restrict__ b1, const float *__restrict__ w2,
+                          const float *__restrict__ b2, const __grid_constant__ HeadConsts cst,
+                          const uint32_t *__restrict__ ids, const uint8_t *__restrict__ is_prefill,
+                          const float *__restrict__ prior_override, int max_slots,
+                          float *__restrict__ lq_state, SlotMeta *__restrict__ meta,
+                          float *__restrict__ post, float *__restrict__ Lout,
+                          uint32_t *__restrict__ err) {
+  using C = WCfg<KB>;
+  constexpr int KBP = C::KBP;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t s0 = smem_u32(smem);
+  const uint32_t full0 = s0 + C::BAR_OFF, empty0 = full0 + 8 * WSTAGES, done = full0 + 16 * WSTAGES;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::BAR_OFF + 16 * WSTAGES + 8);
+  float *b1s = reinterpret_cast<float *>(smem + C::B1_OFF);
+  uint32_t *s_slot = reinterpret_cast<uint32_t *>(smem + C::SLOT_OFF);
+  SlotMeta *s_meta = reinterpret_cast<SlotMeta *>(smem + C::META_OFF);
+  float *s_lq = reinterpret_cast<float *>(smem + C::LQ_OFF);
+  HeadSmem &hs = *reinterpret_cast<HeadSmem *>(smem + C::HC_OFF);
+  float *w2s = reinterpret_cast<float *>(smem + C::W2S_OFF);   // [512][KBP] after the mainloop
+  float *zs = reinterpret_cast<float *>(smem + C::ZS_OFF);     // [2][128][KBP]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const uint32_t r = cluster_rank();
+  const int m0 = (int)(blockIdx.x >> 1) * 2 * WBM + (int)r * WBM;
+  const int k = cst.k;
+
+  if (tid == 0) {
+    for (int i = 0; i < WSTAGES; ++i) {
+      mbar_init(full0 + 8 * i, 1);
+      mbar_init(empty0 + 8 * i, 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_w)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_emb)) : "memory");
+  }
+  if (warp == 0) tmem_alloc_pair(smem_u32(tmem_slot), (uint32_t)WH);
+  tc_fence_before();
+  cluster_sync();                    // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_launch();
+
+  if (warp == 0) {
+    const XPlan xp = xplan_make(off, n, m0, lane);
+    const uint32_t lead_full0 = mapa(full0, 0u);
+    const int pre = kblocks < WSTAGES ? kblocks : WSTAGES;
+    // W1 tiles of the first stages do not depend on an earlier kernel (PDL overlap)
+    if (lane == 0)
+      for (int i = 0; i < pre; ++i) {
+        if (r == 0) mbar_expect_tx(full0 + 8 * i, 2 * WSTAGE);
+        const uint32_t sb = s0 + i * WSTAGE + WA;
+        tma_load_2d_pair(sb, &tmap_w, lead_full0 + 8 * i, i * WBK, (int)r * 128);
+        tma_load_2d_pair(sb + WBH, &tmap_w, lead_full0 + 8 * i, i * WBK, 256 + (int)r * 128);
+      }
+    if (xp.tile_xs) griddep_wait();
+    __syncwarp();
+    for (int i = 0; i < kblocks; ++i) {
+      const int st = i % WSTAGES;
+      const int kc = i * WBK;
+      if (i >= WSTAGES) {
+        if (lane == 0) {
+          mbar_wait(empty0 + 8 * st, ((uint32_t)(i / WSTAGES) & 1u) ^ 1u);
+          if (r == 0) mbar_expect_tx(full0 + 8 * st, 2 * WSTAGE);
+          const uint32_t sb = s0 + st * WSTAGE + WA;
+          tma_load_2d_pair(sb, &tmap_w, lead_full0 + 8 * st, kc, (int)r * 128);
+          tma_load_2d_pair(sb + WBH, &tmap_w, lead_full0 + 8 * st, kc, 256 + (int)r * 128);
+        }
+        __syncwarp();
+      }
+      xplan_issue<true>(xp, lane, s0 + st * WSTAGE, lead_full0 + 8 * st, kc, &tmap_emb, &tmap_emb4,
+                        &tmap_emb32, &tmap_xs, &tmap_xs4, &tmap_xs32);
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && r == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(2 * WBM, 256);
+      for (int i = 0; i < kblocks; ++i) {
+        const int st = i % WSTAGES;
+        mbar_wait(full0 + 8 * st, (uint32_t)(i / WSTAGES) & 1u);
+        tc_fence_after();
+        const uint32_t sa = s0 + st * WSTAGE;
+        const uint64_t da = sw128_kmajor_desc(sa);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint64_t db = sw128_kmajor_desc(sa + WA + h * WBH);
+#pragma unroll
+          for (int kk = 0; kk < WBK / 16; ++kk)
+            umma_bf16_pair(tmem + 256 * h, da + 2 * kk, db + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit_pair(empty0 + 8 * st);
+      }
+      umma_commit_pair(done);
+    }
+    __syncwarp();
+  } else {
+    // b1, head constants and this CTA's slot state (weights and state written by kernels that
+    // completed before the pool kernel passed its own griddep_wait: PDL chain)
+    const int t = tid - 64;
+    for (int v = t; v < WH / 4; v += WT - 64)
+      reinterpret_cast<float4 *>(b1s)[v] = __ldg(reinterpret_cast<const float4 *>(b1) + v);
+    if (t < kMaxBins) {
+      hs.m[t] = cst.m[t];
+      hs.log_stay[t] = cst.log_stay[t];
+      hs.log_move[t] = cst.log_move[t];
+      hs.log_prior[t] = cst.log_prior[t];
+      hs.thr[t] = cst.thr_tab[t];
+    }
+    if (t < WBM) {
+      const int j = m0 + t;
+      uint32_t sl = 0xFFFFFFFFu;
+      if (j < n) {
+        sl = __ldg(ids + j);
+        const bool pref = __ldg(is_prefill + j) != 0;
+        if (sl < (uint32_t)max_slots) {
+          s_meta[t] = meta[sl];
+#pragma unroll
+          for (int b = 0; b < KB; ++b)
+            if (b < k) s_lq[t * KB + b] = lq_state[(int64_t)sl * k + b];
+          sl |= pref ? 0x80000000u : 0u;
+        } else {
+          sl = 0xFFFFFFFFu;
+        }
+      }
+      s_slot[t] = sl;
+    }
+  }
+
+  // ---- epilogue: the pipeline is idle once `done` completes (all MMAs of the pair retired)
+  mbar_wait(done, 0);
+  __syncwarp();
+  tc_fence_after();
+  // W2^T into the idle pipeline buffers: w2s[c][b] = W2[b][c] (b >= k zero), coalesced reads
+  for (int v = tid; v < KBP * WH; v += WT) {
+    const int b = v / WH, c = v - b * WH;
+    w2s[c * KBP + b] = b < k ? __ldg(w2 + (int64_t)b * WH + c) : 0.f;
+  }
+  __syncthreads();
+  {
+    // thread (row, column half): h = ReLU(acc + b1) over 256 columns, z_half = W2 h_half
+    const int g = warp & 3, half = warp >> 2;
+    const int row = 32 * g + lane;
+    float z[KBP];
+#pragma unroll
+    for (int b = 0; b < KBP; ++b) z[b] = 0.f;
+    for (int cc = 0; cc < 256; cc += 32) {
+      const int c0 = 256 * half + cc;
+      uint32_t v[32];
+      tmem_ld32(tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)c0, v);
+#pragma unroll 4
+      for (int q = 0; q < 32; ++q) {
+        const float hq = fmaxf(__uint_as_float(v[q]) + b1s[c0 + q], 0.f);
+        const float4 *wq = reinterpret_cast<const float4 *>(w2s + (c0 + q) * KBP);
+#pragma unroll
+        for (int b4 = 0; b4 < KBP / 4; ++b4) {
+          const float4 w = wq[b4];
+          z[4 * b4] = fmaf(hq, w.x, z[4 * b4]);
+          z[4 * b4 + 1] = fmaf(hq, w.y, z[4 * b4 + 1]);
+          z[4 * b4 + 2] = fmaf(hq, w.z, z[4 * b4 + 2]);
+          z[4 * b4 + 3] = fmaf(hq, w.w, z[4 * b4 + 3]);
+        }
+      }
+    }
+    float4 *zo = reinterpret_cast<float4 *>(zs + (half * WBM + row) * KBP);
+#pragma unroll
+    for (int b4 = 0; b4 < KBP / 4; ++b4) zo[b4] = make_float4(z[4 * b4], z[4 * b4 + 1], z[4 * b4 + 2], z[4 * b4 + 3]);
+  }
+  __syncthreads();
+  // ---- head (row a3): one lane per bin, SEG-lane segments, rows spread over the 8 warps
+  {
+    const int SEG = k <= 16 ? 16 : 32;
+    const int per_warp = 32 / SEG, seg = lane / SEG, b = lane % SEG;
+    for (int base = warp * per_warp; base < WBM; base += (WT / 32) * per_warp) {
+      const int rr = base + seg;
+      const int j = m0 + rr < n ? m0 + rr : n;
+      float z = 0.f;
+      if (j < n && b < k)
+        z = (__ldg(b2 + b) + zs[rr * KBP + b]) + zs[(WBM + rr) * KBP + b];
+      head_seg(j, n, k, SEG, b, z, hs, j < n ? s_slot[rr] : 0xFFFFFFFFu, s_meta[rr],
+               b < KB ? s_lq[rr * KB + (b < KB ? b : 0)] : -INFINITY, prior_override, lq_state,
+               meta, post, Lout, err);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();                    // both CTAs done with TMEM
+  if (warp == 0) tmem_dealloc_pair(tmem, (uint32_t)WH);
+}
+
+// ------------------------------------------------------------------ host
+static int wide_kb(int k) { return k <= 10 ? 10 : k <= 16 ? 16 : k <= 20 ? 20 : 32; }
+
+bool wide_supported(const Ctx &c) {
+  return c.dtype == TRAIL_BF16 && c.H == WH && c.k <= 32 && c.d % WBK == 0;
+}
+
+// AUTO uses the wide kernel from this many requests on (TRAIL_WIDE_MIN overrides; measured
+// crossover against K2c)
+int wide_min_n() {
+  static const int v = [] {
+    const char *e = getenv("TRAIL_WIDE_MIN");
+    const int x = e ? atoi(e) : 0;
+    return x > 0 ? x : 4608;
+  }();
+  return v;
+}
+
+template <int KB>
+static cudaError_t wide_attr() {
+  return cudaFuncSetAttribute(trail_wide_predict_kernel<KB>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, WCfg<KB>::SMEM_TOTAL);
+}
+
+cudaError_t wide_prepare(Ctx &c) {
+  if (!wide_supported(c)) return cudaSuccess;
+  switch (wide_kb(c.k)) {
+    case 10: return wide_attr<10>();
+    case 16: return wide_attr<16>();
+    case 20: return wide_attr<20>();
+    default: return wide_attr<32>();
+  }
+}
+
+cudaError_t launch_wide_predict(Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
+                                const uint32_t *ids, const uint8_t *is_prefill,
+                                const float *prior_override, float *post, float *L,
+                                cudaStream_t s) {
+  if (!c.have_tmaps || !wide_supported(c)) return cudaErrorInvalidValue;
+  if (!ensure_emb_tmaps(c, emb, ld)) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * ((n + 2 * WBM - 1) / (2 * WBM)));
+  cfg.blockDim = dim3(WT);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeClusterDimension;
+  attr[na].val.clusterDim.x = 2;
+  attr[na].val.clusterDim.y = 1;
+  attr[na].val.clusterDim.z = 1;
+  ++na;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+#define TRAIL_WIDE(KB)                                                                            \
+  cfg.dynamicSmemBytes = WCfg<KB>::SMEM_TOTAL;                                                    \
+  return cudaLaunchKernelEx(&cfg, trail_wide_predict_kernel<KB>, c.tmap_emb, c.tmap_emb4,        \
+                            c.tmap_emb32, c.tmap_xs1, c.tmap_xs4, c.tmap_xs32, c.tmap_w128, off, \
+                            n, c.d / WBK, (const float *)c.b1, (const float *)c.w2,              \
+                            (const float *)c.b2, c.host_consts, ids, is_prefill, prior_override, \
+                            c.cfg.max_slots, c.lq, c.meta, post, L, c.dev_err)
+  switch (wide_kb(c.k)) {
+    case 10: TRAIL_WIDE(10);
+    case 16: TRAIL_WIDE(16);
+    case 20: TRAIL_WIDE(20);
+    default: TRAIL_WIDE(32);
+  }
+#undef TRAIL_WIDE
+}
+
+}  // namespace trail

@@ -65,6 +65,15 @@ void plan_l1(const Ctx &c, int n, int *mode, int *bn, int *splits) {
   int m = c.cfg.l1_mode;
   if (c.dtype == TRAIL_F32) m = TRAIL_L1_GEMV;
   else if (m == TRAIL_L1_AUTO) m = (n <= kGemvMaxN) ? TRAIL_L1_GEMV : TRAIL_L1_UMMA;
+  if (m == TRAIL_L1_UMMA && c.cfg.l1_mode == TRAIL_L1_AUTO && wide_supported(c) && n >= wide_min_n())
+    m = TRAIL_L1_WIDE;
+  if (m == TRAIL_L1_WIDE && !wide_supported(c)) m = TRAIL_L1_UMMA;
+  if (m == TRAIL_L1_WIDE) {
+    *mode = TRAIL_L1_WIDE;
+    *bn = 512;
+    *splits = 1;
+    return;
+  }
   if (m == TRAIL_L1_UMMA) {
     *mode = TRAIL_L1_UMMA;
     *bn = 128;
@@ -199,7 +208,7 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
   if (g.max_slots <= 0 || g.max_requests <= 0 || g.max_sched < 0) return TRAIL_ERR_INVALID;
   if (g.max_requests > (1 << 18)) return TRAIL_ERR_INVALID;   // K1 offset search bound
   if (g.world_size < 1) return TRAIL_ERR_INVALID;
-  if (g.l1_mode < 0 || g.l1_mode > 3) return TRAIL_ERR_INVALID;
+  if (g.l1_mode < 0 || g.l1_mode > 4) return TRAIL_ERR_INVALID;
   if (g.l1_mode >= TRAIL_L1_UMMA && g.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
   if ((int64_t)g.max_sched * g.world_size > (1 << 26)) return TRAIL_ERR_INVALID;
   const int k = g.k;
@@ -319,7 +328,8 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
     return fail(TRAIL_ERR_CUDA);
   if (umma_prepare(c) != cudaSuccess || head_prepare(c) != cudaSuccess ||
       pool_prepare() != cudaSuccess ||
-      fused_prepare(c) != cudaSuccess || select_prepare(c) != cudaSuccess)
+      fused_prepare(c) != cudaSuccess || wide_prepare(c) != cudaSuccess ||
+      select_prepare(c) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(TRAIL_ERR_CUDA);
   *out = h;
@@ -365,7 +375,7 @@ trail_status trail_trace_read(trail_handle h, uint64_t *host_out, int32_t max_ct
 }
 
 trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode) {
-  if (!h || l1_mode < 0 || l1_mode > 3) return TRAIL_ERR_INVALID;
+  if (!h || l1_mode < 0 || l1_mode > 4) return TRAIL_ERR_INVALID;
   if (l1_mode >= TRAIL_L1_UMMA && h->c.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
   h->c.cfg.l1_mode = l1_mode;
   return TRAIL_OK;
@@ -403,11 +413,18 @@ trail_status trail_predict_step(trail_handle h, const void *emb, int64_t emb_ld,
   cudaStream_t s = (cudaStream_t)stream;
   int mode, bn, splits;
   plan_l1(c, n, &mode, &bn, &splits);
-  if (mode != TRAIL_L1_UMMA && (size_t)splits * n * c.H > c.partial_elems)
+  if (mode != TRAIL_L1_UMMA && mode != TRAIL_L1_WIDE && (size_t)splits * n * c.H > c.partial_elems)
     return TRAIL_ERR_CAPACITY;
   {
     ProfScope p(c, TRAIL_K_POOL, s);
-    TRAIL_CUDA(launch_pool(c, emb, emb_ld, row_offsets, n, mode == TRAIL_L1_UMMA ? 0 : 1, s));
+    TRAIL_CUDA(launch_pool(c, emb, emb_ld, row_offsets, n,
+                           (mode == TRAIL_L1_UMMA || mode == TRAIL_L1_WIDE) ? 0 : 1, s));
+  }
+  if (mode == TRAIL_L1_WIDE) {   // layer 1 + layer 2 + head, CTA pairs over the whole hidden width
+    ProfScope p(c, TRAIL_K_UMMA, s);
+    TRAIL_CUDA(launch_wide_predict(c, emb, emb_ld, row_offsets, n, request_ids, is_prefill,
+                                   prior_override, posteriors, expected_remaining, s));
+    return TRAIL_OK;
   }
   if (mode == TRAIL_L1_UMMA) {   // layer 1 + layer 2 + head in one kernel
     ProfScope p(c, TRAIL_K_UMMA, s);

@@ -137,6 +137,14 @@ cudaError_t launch_fused_predict(Ctx &c, const void *emb, int64_t ld, const int3
                                  int splits, const uint32_t *ids,
                                  const uint8_t *is_prefill, const float *prior_override,
                                  float *post, float *L, cudaStream_t s);
+bool ensure_emb_tmaps(Ctx &c, const void *emb, int64_t ld);
+bool wide_supported(const Ctx &c);
+int wide_min_n();
+cudaError_t wide_prepare(Ctx &c);
+cudaError_t launch_wide_predict(Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
+                                const uint32_t *ids, const uint8_t *is_prefill,
+                                const float *prior_override, float *post, float *L,
+                                cudaStream_t s);
 cudaError_t select_prepare(Ctx &c);
 cudaError_t select_radix_prepare();
 int select_radix_capacity();

@@ -45,6 +45,10 @@ CASES = [
     ("bf16", 200, 1024, 256, 20, 3, 0.1),
     ("bf16", 2000, 512, 512, 10, 2, 0.0),    # fused kernel, no split (S = 1), 16 M tiles
     ("bf16", 129, 8192, 512, 20, 2, 0.5),    # fused kernel, 16-CTA clusters
+    ("bf16", 300, 4096, 512, 10, 4, 0.2),    # wide CTA-pair kernel: 2 pairs, ragged tail
+    ("bf16", 129, 8192, 512, 20, 4, 0.5),    # wide, config 4 width, peer CTA 1 row
+    ("bf16", 1000, 1024, 512, 32, 4, 0.1),   # wide, k = 32
+    ("bf16", 64, 512, 512, 16, 4, 0.0),      # wide, 8 K blocks (< 2 laps of the ring), empty peer
     ("f32", 64, 4096, 512, 10, 0, 0.0),      # config 1 shape (fp32 GEMV)
     ("f32", 9, 1024, 256, 3, 1, 1.0),
 ]
