@@ -51,6 +51,16 @@ CONFIGS = {
 }
 
 
+def sm_max_mhz():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            v = json.load(f).get("sm_max_mhz")
+        if v:
+            return float(v)
+    return 1965.0   # B200 clocks.max.sm (B200_PROFILING.md)
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -298,7 +308,15 @@ def run_ours(args, cfg):
         ach_tf = flops / t_s / 1e12
         # at n = 512 the contraction sits at the bf16 ridge (I = 254 vs 259 flop/B): report
         # the bound whose fraction is larger
-        if dom == "umma" and ach_tf / tf_sust > ach_bw / hbm:
+        # fp32 FFMA peak of the CUDA cores (the GEMV kernel's unit): 148 SMs x 128 FP32
+        # lanes x 2 flop x SM clock; its ridge is ~11 flop/B
+        alu_tf = torch.cuda.get_device_properties(device).multi_processor_count * 128 * 2 * \
+            sm_max_mhz() * 1e6 / 1e12
+        if dom == "gemv" and ach_tf / alu_tf > ach_bw / hbm:
+            roof = {"bound": "alu", "achieved": ach_tf, "peak": alu_tf, "unit": "TFLOP/s",
+                    "frac": ach_tf / alu_tf,
+                    "peak_note": "fp32 FFMA: SMs x 128 lanes x 2 flop x max SM clock"}
+        elif dom == "umma" and ach_tf / tf_sust > ach_bw / hbm:
             roof = {"bound": "tensor", "achieved": ach_tf, "peak": tf_sust, "unit": "TFLOP/s",
                     "frac": ach_tf / tf_sust}
         else:

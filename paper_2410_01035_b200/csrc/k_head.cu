@@ -15,9 +15,9 @@
 // The state is the LOG posterior in fp32 (reading D-22): the same real-number recursion as
 // P:220-222 without the underflow of a linear fp32 filter under confident, contradictory
 // observations.  Lane i of the warp owns bin i (k <= 32); the 512 hidden values are spread
-// 16 per lane as 4 float4 chunks (coalesced 512-byte rows of the partials).  W2 is staged
-// in shared memory once per CTA; the reduction over splits runs in a fixed order, so
-// results are bit-reproducible.
+// over the warps of the request's CTA, 4 per lane (coalesced 512-byte rows of the partials);
+// layer 2 per warp + a fixed-order sum of the warps' bin partials; the reduction over splits
+// runs in a fixed order, so results are bit-reproducible.
 #include <math.h>
 
 #include "trail_internal.cuh"
@@ -33,7 +33,7 @@ __device__ __forceinline__ float logaddexp_f(float a, float b) {
 }  // namespace
 
 template <int HC>  // hidden = 128 * HC
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
 trail_head_kernel(const float *__restrict__ partial, int splits, int n,
                   const float *__restrict__ b1, const float *__restrict__ w2,
                   const float *__restrict__ b2, const HeadConsts *__restrict__ cst,
@@ -42,70 +42,79 @@ trail_head_kernel(const float *__restrict__ partial, int splits, int n,
                   float *__restrict__ lq_state, SlotMeta *__restrict__ meta,
                   float *__restrict__ post, float *__restrict__ Lout, uint32_t *__restrict__ err) {
   constexpr int H = 128 * HC;
-  extern __shared__ float w2s[];  // [k][H]
+  __shared__ float zs[HC][32];
   const int k = cst->k;
-  for (int i = threadIdx.x; i < k * H / 4; i += blockDim.x)
-    reinterpret_cast<float4 *>(w2s)[i] = __ldg(reinterpret_cast<const float4 *>(w2) + i);
-  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // one CTA per request, warp c owns hidden units [128 c, 128 c + 128) (4 per lane): the
+  // split-K sum of those units has all `splits` loads of a lane in flight at once
+  const int c = warp;
+  const float4 bias1 = c < HC ? __ldg(reinterpret_cast<const float4 *>(b1 + c * 128) + lane)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
   griddep_wait();      // partials from layer 1, slot state from the previous step
   griddep_launch();
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool active = lane < k;
-  const float m_i = active ? cst->m[lane] : 0.f;
-  const float lstay = active ? cst->log_stay[lane] : -INFINITY;
-  const float lmove = active ? cst->log_move[lane] : -INFINITY;
-  const float lpi = active ? cst->log_prior[lane] : -INFINITY;
-  const float bias2 = active ? __ldg(b2 + lane) : 0.f;
-  float4 bias1[HC];
+  for (int j = blockIdx.x; j < n; j += gridDim.x) {
+    // ---- h = ReLU(sum_s partial + b1) for my 4 hidden units, fixed split order
+    if (c < HC) {
+      float4 h = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 *src = reinterpret_cast<const float4 *>(partial + (int64_t)j * H + c * 128) + lane;
+      const int64_t sstride = (int64_t)n * H / 4;
+      int sp = 0;
+      for (; sp + 8 <= splits; sp += 8) {
+        float4 v[8];
 #pragma unroll
-  for (int c = 0; c < HC; ++c)
-    bias1[c] = __ldg(reinterpret_cast<const float4 *>(b1 + c * 128) + lane);
-
-  const int warps_total = gridDim.x * (blockDim.x >> 5);
-  for (int j = blockIdx.x * (blockDim.x >> 5) + warp; j < n; j += warps_total) {
-    const uint32_t slot = __ldg(ids + j);
-    if (slot >= (uint32_t)max_slots) {
-      if (lane == 0) atomicOr(err, TRAIL_DEV_BAD_ID);
-      if (active && post) post[(int64_t)j * k + lane] = NAN;
-      if (lane == 0 && Lout) Lout[j] = NAN;
-      continue;
-    }
-    // ---- h = ReLU(sum_s partial + b1), fixed split order
-    float4 h[HC];
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(src + (sp + u) * sstride);
 #pragma unroll
-    for (int c = 0; c < HC; ++c) h[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < splits; ++s) {
-      const float4 *src = reinterpret_cast<const float4 *>(partial + ((int64_t)s * n + j) * H);
-#pragma unroll
-      for (int c = 0; c < HC; ++c) {
-        const float4 v = __ldcs(src + c * 32 + lane);
-        h[c].x += v.x; h[c].y += v.y; h[c].z += v.z; h[c].w += v.w;
+        for (int u = 0; u < 8; ++u) { h.x += v[u].x; h.y += v[u].y; h.z += v[u].z; h.w += v[u].w; }
       }
-    }
-#pragma unroll
-    for (int c = 0; c < HC; ++c) {
-      h[c].x = fmaxf(h[c].x + bias1[c].x, 0.f);
-      h[c].y = fmaxf(h[c].y + bias1[c].y, 0.f);
-      h[c].z = fmaxf(h[c].z + bias1[c].z, 0.f);
-      h[c].w = fmaxf(h[c].w + bias1[c].w, 0.f);
-    }
-    // ---- z = W2 h + b2 ; lane b keeps z_b
-    float z = -INFINITY;
-    for (int b = 0; b < k; ++b) {
-      const float4 *wr = reinterpret_cast<const float4 *>(w2s + b * H);
-      float acc = 0.f;
-#pragma unroll
-      for (int c = 0; c < HC; ++c) {
-        const float4 w = wr[c * 32 + lane];
-        acc = fmaf(w.x, h[c].x, acc);
-        acc = fmaf(w.y, h[c].y, acc);
-        acc = fmaf(w.z, h[c].z, acc);
-        acc = fmaf(w.w, h[c].w, acc);
+      for (; sp < splits; ++sp) {
+        const float4 v = __ldcs(src + sp * sstride);
+        h.x += v.x; h.y += v.y; h.z += v.z; h.w += v.w;
       }
-      acc = warp_sum(acc);
-      if (lane == b) z = acc + bias2;
+      h.x = fmaxf(h.x + bias1.x, 0.f);
+      h.y = fmaxf(h.y + bias1.y, 0.f);
+      h.z = fmaxf(h.z + bias1.z, 0.f);
+      h.w = fmaxf(h.w + bias1.w, 0.f);
+      // ---- layer 2 over my units: every lane forms its 32 per-bin partial dots (bins >= k
+      //      zero), one warp reduce-scatter (31 shuffles) leaves bin b's chunk sum on lane b
+      float zp[32];
+#pragma unroll
+      for (int b = 0; b < 32; ++b) {
+        float acc = 0.f;
+        if (b < k) {
+          const float4 w = __ldg(reinterpret_cast<const float4 *>(w2 + (int64_t)b * H + c * 128) + lane);
+          acc = fmaf(w.x, h.x, fmaf(w.y, h.y, fmaf(w.z, h.z, w.w * h.w)));
+        }
+        zp[b] = acc;
+      }
+#pragma unroll
+      for (int step = 0; step < 5; ++step) {
+        const int half = 16 >> step;
+        const bool upper = (lane & half) != 0;
+#pragma unroll
+        for (int i = 0; i < half; ++i) {
+          const float a = zp[i], b = zp[i + half];
+          zp[i] = (upper ? b : a) + __shfl_xor_sync(0xffffffffu, upper ? a : b, half);
+        }
+      }
+      zs[c][lane] = zp[0];    // lane l holds bin 16 b4 + 8 b3 + 4 b2 + 2 b1 + b0 = l
     }
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t slot = __ldg(ids + j);
+      if (slot >= (uint32_t)max_slots) {
+        if (lane == 0) atomicOr(err, TRAIL_DEV_BAD_ID);
+        if (active && post) post[(int64_t)j * k + lane] = NAN;
+        if (lane == 0 && Lout) Lout[j] = NAN;
+      } else {
+        const float m_i = active ? cst->m[lane] : 0.f;
+        const float lstay = active ? cst->log_stay[lane] : -INFINITY;
+        const float lmove = active ? cst->log_move[lane] : -INFINITY;
+        const float lpi = active ? cst->log_prior[lane] : -INFINITY;
+        float z = active ? __ldg(b2 + lane) : 0.f;
+#pragma unroll
+        for (int cc = 0; cc < HC; ++cc) z += zs[cc][lane];
+        if (!active) z = -INFINITY;
     // ---- log-softmax over the k lanes
     const float zmax = warp_max(z);
     const float se = warp_sum(active ? expf(z - zmax) : 0.f);
@@ -153,6 +162,9 @@ trail_head_kernel(const float *__restrict__ partial, int splits, int n,
       meta[slot] = mt;
       if (Lout) Lout[j] = L;
     }
+      }
+    }
+    __syncthreads();   // zs reused by the next request of this CTA
   }
 }
 
@@ -160,12 +172,12 @@ cudaError_t launch_head(const Ctx &c, int n, int splits, const uint32_t *ids,
                         const uint8_t *is_prefill, const float *prior_override, float *post,
                         float *L, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  // 4 requests per CTA: >= one CTA per SM already at n = 512 (latency-bound kernel)
+  // one CTA per request (a warp per 128 hidden units), up to 8 CTAs per SM
   const int warps = 4;
-  int blocks = (n + warps - 1) / warps;
+  int blocks = n;
   const int cap = c.num_sms * 8;
   if (blocks > cap) blocks = cap;
-  const size_t smem = (size_t)c.k * c.H * sizeof(float);
+  const size_t smem = 0;
 #define TRAIL_HEAD(HC)                                                                        \
   return launch_k(trail_head_kernel<HC>, dim3(blocks), dim3(warps * 32), smem, s, c.partial,  \
                   splits, n, c.b1, c.w2, c.b2, c.consts, ids, is_prefill, prior_override,     \
@@ -179,16 +191,6 @@ cudaError_t launch_head(const Ctx &c, int n, int splits, const uint32_t *ids,
 #undef TRAIL_HEAD
 }
 
-cudaError_t head_prepare(Ctx &c) {
-  const int smem = c.k * c.H * (int)sizeof(float);
-  cudaError_t e = cudaSuccess;
-  if (smem > 48 * 1024) {
-    e = cudaFuncSetAttribute(trail_head_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(trail_head_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(trail_head_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(trail_head_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  }
-  return e;
-}
+cudaError_t head_prepare(Ctx &) { return cudaSuccess; }   // no dynamic shared memory
 
 }  // namespace trail

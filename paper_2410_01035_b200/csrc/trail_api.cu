@@ -81,10 +81,15 @@ void plan_l1(const Ctx &c, int n, int *mode, int *bn, int *splits) {
     return;
   }
   if (m == TRAIL_L1_GEMV) {
-    const int ctas_x = c.H / 16;
-    const int vec = c.dtype == TRAIL_BF16 ? 8 : 4;
-    int s = std::max(1, (2 * c.num_sms) / ctas_x);
-    s = std::min(s, std::max(1, c.d / (vec * 32)));
+    // about one CTA per SM (64 hidden rows x one K range each); K ranges a multiple of 8
+    // elements and small enough that both operand slices fit in shared memory
+    const int ctas_x = c.H / 64;
+    int s = std::max(1, c.num_sms / ctas_x);
+    const int kmax = (200 * 1024 - 512) / (128 * (int)c.esize) - 16;
+    s = std::max(s, (c.d + kmax - 1) / kmax);
+    s = std::min(s, std::max(1, c.d / 8));
+    const int kchunk = ((c.d + s - 1) / s + 7) / 8 * 8;
+    s = (c.d + kchunk - 1) / kchunk;
     *mode = TRAIL_L1_GEMV;
     *bn = 0;
     *splits = s;
@@ -327,7 +332,7 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
       cudaMemset(c.xs, 0, (size_t)g.max_requests * c.d * c.esize) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
   if (umma_prepare(c) != cudaSuccess || head_prepare(c) != cudaSuccess ||
-      pool_prepare() != cudaSuccess ||
+      pool_prepare() != cudaSuccess || gemv_prepare() != cudaSuccess ||
       fused_prepare(c) != cudaSuccess || wide_prepare(c) != cudaSuccess ||
       select_prepare(c) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
@@ -417,8 +422,8 @@ trail_status trail_predict_step(trail_handle h, const void *emb, int64_t emb_ld,
     return TRAIL_ERR_CAPACITY;
   {
     ProfScope p(c, TRAIL_K_POOL, s);
-    TRAIL_CUDA(launch_pool(c, emb, emb_ld, row_offsets, n,
-                           (mode == TRAIL_L1_UMMA || mode == TRAIL_L1_WIDE) ? 0 : 1, s));
+    // decode rows are gathered from emb by every layer-1 kernel except the unfused GEMM
+    TRAIL_CUDA(launch_pool(c, emb, emb_ld, row_offsets, n, mode == TRAIL_L1_UMMA_UNFUSED ? 1 : 0, s));
   }
   if (mode == TRAIL_L1_WIDE) {   // layer 1 + layer 2 + head, CTA pairs over the whole hidden width
     ProfScope p(c, TRAIL_K_UMMA, s);
@@ -435,7 +440,7 @@ trail_status trail_predict_step(trail_handle h, const void *emb, int64_t emb_ld,
   }
   if (mode == TRAIL_L1_GEMV) {
     ProfScope p(c, TRAIL_K_GEMV, s);
-    TRAIL_CUDA(launch_gemv_l1(c, n, splits, s));
+    TRAIL_CUDA(launch_gemv_l1(c, emb, emb_ld, row_offsets, n, splits, s));
   } else {
     ProfScope p(c, TRAIL_K_UMMA, s);
     TRAIL_CUDA(launch_umma_l1(c, n, bn, splits, s));

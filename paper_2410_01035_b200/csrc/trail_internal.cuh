@@ -113,7 +113,9 @@ cudaError_t launch_pool(const Ctx &c, const void *emb, int64_t ld, const int32_t
 int pool_grid(const Ctx &c);
 bool pool_use_bulk();
 cudaError_t pool_prepare();
-cudaError_t launch_gemv_l1(const Ctx &c, int n, int splits, cudaStream_t s);
+cudaError_t gemv_prepare();
+cudaError_t launch_gemv_l1(const Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
+                           int splits, cudaStream_t s);
 cudaError_t launch_umma_l1(const Ctx &c, int n, int bn, int splits, cudaStream_t s);
 cudaError_t launch_head(const Ctx &c, int n, int splits, const uint32_t *ids,
                         const uint8_t *is_prefill, const float *prior_override,
