@@ -227,9 +227,12 @@ TRAIL_API trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode);
 
 /* Optional host-side hint: the number of embedding rows (the flat batch's token count,
  * row_offsets[n] - row_offsets[0]) of the next trail_predict_step calls; 0 = unknown (the
- * default).  It only selects the pooling kernel variant (bulk-copy streaming for
- * prefill-heavy batches, P:570 burst shape); results are bit-identical either way.  Kept
- * until changed.  Errors: TRAIL_ERR_INVALID (rows < 0). */
+ * default).  It only selects the pooling kernel variant and grid (bulk-copy streaming for
+ * prefill-heavy batches, P:570 burst shape; more row chunks for large mixed batches).  The
+ * fp32 prompt sums are combined over row chunks in a fixed order, so results are
+ * deterministic for a given hint; between hints the pooled means of prompts that cross a
+ * chunk boundary may differ in the last bit (fp32 summation grouping).  Kept until
+ * changed.  Errors: TRAIL_ERR_INVALID (rows < 0). */
 TRAIL_API trail_status trail_set_rows_hint(trail_handle h, int64_t rows);
 
 /* Which layer-1 kernel trail_predict_step uses for n requests, and its split-K factor. */
