@@ -127,6 +127,17 @@ def bayes_update_log(lq_prev: np.ndarray, logp: np.ndarray, T: np.ndarray) -> np
     return lnum - (m2 + np.log(np.exp(lnum - m2).sum(axis=-1, keepdims=True)))
 
 
+def time_update(q_prev: np.ndarray, T: np.ndarray, steps: int) -> np.ndarray:
+    """Predict-every-K variant ("making predictions ... every K iterations"; SURVEY
+    §8(f)3): between two observations only the transition acts, q <- normalise(T q), once
+    per iteration (readings D-1/D-4; no likelihood term, reading D-25)."""
+    q = np.asarray(q_prev, dtype=np.float64)
+    for _ in range(int(steps)):
+        q = q @ T.T
+        q = q / q.sum(axis=-1, keepdims=True)
+    return q
+
+
 def expected_length(q: np.ndarray, m: np.ndarray) -> np.ndarray:
     """L_t = sum_i q^(t)(i) m_i."""
     return q @ m
@@ -225,6 +236,24 @@ class TrailOracle:
         L = expected_length(q, self.m)
         st.q[ids] = q
         st.L[ids] = L
+        return q, L
+
+    def time_update(self, request_ids: np.ndarray, steps: int) -> Tuple[np.ndarray, np.ndarray]:
+        """Iterations without an observation: observed slots get `steps`
+        transitions, age a += steps (D-11), L refreshed; unobserved slots are untouched and
+        report the prior pi and E_pi[L] (D-24)."""
+        ids = np.asarray(request_ids, dtype=np.int64)
+        st = self.state
+        q = np.broadcast_to(self.prior, (ids.shape[0], self.k)).copy()
+        L = np.full(ids.shape[0], self.prior_L)
+        seen = st.seen[ids]
+        if seen.any() and steps > 0:
+            si = ids[seen]
+            st.q[si] = time_update(st.q[si], self.T, steps)
+            st.age[si] += int(steps)
+            st.L[si] = expected_length(st.q[si], self.m)
+        q[seen] = st.q[ids[seen]]
+        L[seen] = st.L[ids[seen]]
         return q, L
 
     # ------------------------------------------------------------------ schedule

@@ -255,3 +255,41 @@ def test_oracle_step_semantics():
     key, forced = o.keys_and_forced(np.array([1, 3, 5]), np.array([1, 1, 0]))
     assert key[2] == pytest.approx(256.0) and not forced[2]
     assert list(forced[:2]) == [bool(1 >= t) for t in thr0]
+
+
+# ----------------------------------------------------------------------------- time update
+def test_time_update_closed_form_matrix_power_and_state():
+    """Predict-every-K (reading D-25): between observations only T acts.  Pinned by
+    (1) the L - 1 closed form per iteration (equal widths: L' = (L - 1 + q_0/2)/(1 - q_0/w),
+    derived in DESIGN.md §4 — with no likelihood term it applies directly), (2) K
+    normalised steps = one normalised application of the matrix power T^K (normalisation
+    commutes with the linear map up to scale), (3) the oracle's state bookkeeping: age
+    advances by K, unobserved slots keep the prior and E_pi[L] (D-24)."""
+    e = W.paper_bin_edges(10)
+    m, T, w = R.bin_midpoints(e), R.transition_matrix(e), 51.2
+    rs = np.random.default_rng(11)
+    q = rs.dirichlet(np.ones(10), size=32)
+    q[:16, 0] = 0.0
+    q /= q.sum(axis=1, keepdims=True)
+    L, q0 = R.expected_length(q, m), q[:, 0]
+    np.testing.assert_allclose(R.expected_length(R.time_update(q, T, 1), m),
+                               (L - 1 + q0 / 2) / (1 - q0 / w), rtol=1e-12)
+    for K in (1, 2, 5, 17):
+        direct = q @ np.linalg.matrix_power(T, K).T
+        direct /= direct.sum(axis=1, keepdims=True)
+        np.testing.assert_allclose(R.time_update(q, T, K), direct, rtol=1e-10, atol=1e-15)
+    # mass concentrated away from the lowest bin: exactly one length unit per iteration
+    qq = np.zeros((1, 10))
+    qq[0, 5] = 1.0
+    assert R.expected_length(R.time_update(qq, T, 3), m)[0] == pytest.approx(
+        R.expected_length(qq, m)[0] - 3, abs=1e-9)
+    # oracle state
+    w_ = W.make_weights(64, 128, 10, "f32", seed=3)
+    o = R.TrailOracle(w_["W1"], w_["b1"], w_["W2"], w_["b2"], w_["edges"], 0.8, 8, x_dtype="f32")
+    emb, off, pref = W.make_step_inputs(4, 64, "f32", prefill_frac=1.0, seed=4)
+    qa, La = o.predict_step(W.decode(emb, "f32"), off, np.arange(4), pref)
+    qt, Lt = o.time_update(np.array([0, 1, 2, 3, 6]), 3)
+    np.testing.assert_allclose(qt[:4], R.time_update(qa, o.T, 3), rtol=1e-12)
+    assert np.all(o.state.age[:4] == 3) and o.state.age[6] == 0 and not o.state.seen[6]
+    np.testing.assert_allclose(qt[4], np.full(10, 0.1))
+    assert Lt[4] == pytest.approx(256.0)
