@@ -133,6 +133,20 @@ TRAIL_API trail_status trail_predict_step(trail_handle h, const void *emb, int64
                                 int32_t n, float *posteriors, float *expected_remaining,
                                 trail_stream stream);
 
+/* Iterations without an observation — the "predict every K iterations" variant (P:717,
+ * SURVEY §8(f)3).  For each listed slot that has been observed: the transition alone acts,
+ * q <- normalise(T q) (readings D-1/D-4, log domain D-22), `steps` times; the
+ * age a advances by `steps` (the request kept generating, D-11) and L_t is refreshed, so
+ * the next trail_predict_step / trail_schedule_step see the propagated state (reading
+ * D-25).  Never-observed slots are untouched and report the prior pi and E_pi[L] (D-24).
+ *   request_ids [n] device slot ids;  steps >= 0 (0 = only report the state);
+ *   posteriors [n][k] / expected_remaining [n] fp32 device outputs, may be NULL.
+ * Enqueued on `stream`.  Errors: TRAIL_ERR_INVALID (n < 0, steps < 0, NULL ids with n > 0);
+ * a slot id >= max_slots sets TRAIL_DEV_BAD_ID and NaN outputs for that request. */
+TRAIL_API trail_status trail_time_update(trail_handle h, const uint32_t *request_ids, int32_t n,
+                                         int32_t steps, float *posteriors,
+                                         float *expected_remaining, trail_stream stream);
+
 /* Next-batch selection: limited-preemption SPRPT under a KV-block budget (P:171, P:394,
  * P:570).  Inputs are THIS rank's live requests (running + waiting):
  *   request_ids  [n] slot ids;  arrival_seq [n] arrival order (FCFS tie-break),

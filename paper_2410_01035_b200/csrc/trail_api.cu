@@ -453,6 +453,20 @@ trail_status trail_predict_step(trail_handle h, const void *emb, int64_t emb_ld,
   return TRAIL_OK;
 }
 
+trail_status trail_time_update(trail_handle h, const uint32_t *request_ids, int32_t n,
+                               int32_t steps, float *posteriors, float *expected_remaining,
+                               trail_stream stream) {
+  if (!h || n < 0 || steps < 0) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (n == 0) return TRAIL_OK;
+  if (!request_ids) return TRAIL_ERR_INVALID;
+  if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  ProfScope p(c, TRAIL_K_HEAD, s);
+  TRAIL_CUDA(launch_time_update(c, request_ids, n, steps, posteriors, expected_remaining, s));
+  return TRAIL_OK;
+}
+
 trail_status trail_schedule_pack(trail_handle h, const uint32_t *request_ids,
                                  const uint32_t *arrival_seq, const int32_t *kv_blocks,
                                  const uint8_t *is_running, int32_t n, void *records,

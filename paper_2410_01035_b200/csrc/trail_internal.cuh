@@ -126,6 +126,8 @@ cudaError_t launch_pack(const Ctx &c, const uint32_t *ids, const uint32_t *arriv
 cudaError_t launch_select(const Ctx &c, const Record *rec, int n, int64_t budget, int max_run,
                           uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
                           cudaStream_t s);
+cudaError_t launch_time_update(const Ctx &c, const uint32_t *ids, int n, int steps, float *post,
+                               float *L, cudaStream_t s);
 cudaError_t launch_release(const Ctx &c, const uint32_t *ids, int n, cudaStream_t s);
 cudaError_t launch_read_state(const Ctx &c, const uint32_t *ids, int n, float *L, uint32_t *age,
                               uint32_t *thr, uint8_t *seen, float *post, cudaStream_t s);

@@ -80,6 +80,7 @@ _SIGS = {
                             ctypes.POINTER(ctypes.c_int64), _I32], _I32),
     "trail_set_l1_mode": ([_P, _I32], _I32),
     "trail_set_rows_hint": ([_P, _I64], _I32),
+    "trail_time_update": ([_P, _P, _I32, _I32, _P, _P, _P], _I32),
     "trail_trace_enable": ([_P, _I32], _I32),
     "trail_trace_read": ([_P, _P, _I32], _I32),
     "trail_plan_l1": ([_P, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)], _I32),
@@ -237,6 +238,13 @@ def trail_set_l1_mode(h, mode: int) -> None:
     _check("trail_set_l1_mode", _lib().trail_set_l1_mode(h, int(mode)))
 
 
+def trail_time_update(h, request_ids, n: int, steps: int, posteriors, expected_remaining,
+                      stream=None) -> None:
+    _check("trail_time_update", _lib().trail_time_update(
+        h, _ptr(request_ids), int(n), int(steps), _ptr(posteriors), _ptr(expected_remaining),
+        _stream(stream)))
+
+
 def trail_set_rows_hint(h, rows: int) -> None:
     _check("trail_set_rows_hint", _lib().trail_set_rows_hint(h, int(rows)))
 
@@ -312,6 +320,12 @@ class Trail:
             self._rows_hint = rows
         trail_predict_step(self.h, emb, emb.shape[1] if emb.dim() == 2 else self.d, row_offsets,
                            request_ids, is_prefill, prior_override, n, self.post, self.L, stream)
+        return self.post[:n], self.L[:n]
+
+    def time_update(self, request_ids, steps: int, stream=None):
+        """Iterations without an observation (predict every K iterations)."""
+        n = int(request_ids.shape[0])
+        trail_time_update(self.h, request_ids, n, steps, self.post, self.L, stream)
         return self.post[:n], self.L[:n]
 
     def schedule(self, request_ids, arrival_seq, kv_blocks, is_running, kv_budget: int,

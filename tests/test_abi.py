@@ -104,6 +104,8 @@ def test_null_handle_calls_are_invalid(lib):
     assert lib.trail_predict_step(None, None, 0, None, None, None, None, 1, None, None, None) == -1
     assert lib.trail_schedule_step(None, None, None, None, None, 0, 0, 0, None, None, None, None,
                                    None) == -1
+    assert lib.trail_time_update(None, None, 1, 1, None, None, None) == -1
+    assert lib.trail_set_rows_hint(None, 0) == -1
     assert lib.trail_destroy(None) == -1
 
 

@@ -412,3 +412,52 @@ def test_cuda_graph_capture_matches_eager():
                     t.counts.cpu().numpy().copy()))
     for a, bb in zip(res[0], res[1]):
         np.testing.assert_array_equal(a, bb)
+
+
+# ----------------------------------------------------------------------------- time update
+@pytest.mark.parametrize("dtype,n,d,k", [("bf16", 200, 4096, 10), ("f32", 48, 1024, 20),
+                                         ("bf16", 37, 512, 32)])
+def test_time_update_predict_every_k(dtype, n, d, k):
+    """Predict every K iterations: observed requests get a predict step, the rest
+    only the transition (trail_time_update, K6).  Posteriors, L, age and the schedule keys
+    match the oracle after a mixed sequence of gaps; unobserved slots report the prior."""
+    from paper_2410_01035_b200.trail import trail_time_update
+    edges = W.paper_bin_edges(k) if k != 20 else W.paper_bin_edges(20, 1024.0)
+    w = W.make_weights(d, 512 if d >= 1024 else 128, k, dtype, edges=edges, seed=31)
+    t, o = make_pair(w, 0.8, n + 8, n, n + 8, dtype)
+    ids = np.arange(n, dtype=np.uint32)
+    emb, off, pref = W.make_step_inputs(n, d, dtype, prefill_frac=1.0, seed=32)
+    gpu_predict(t, emb, off, ids, pref)
+    oracle_predict(o, emb, off, ids, pref, dtype)
+    rs = np.random.default_rng(33)
+    for it in range(6):
+        obs = rs.random(n) < 0.4
+        steps = int(rs.integers(1, 5))
+        lag = ids[~obs]
+        if lag.size:
+            post = torch.empty((lag.size, k), dtype=torch.float32, device="cuda")
+            Lg = torch.empty(lag.size, dtype=torch.float32, device="cuda")
+            trail_time_update(t.h, dev(lag), lag.size, steps, post, Lg)
+            torch.cuda.synchronize()
+            qo, Lo = o.time_update(lag, steps)
+            assert_predict_close(post.cpu().numpy().astype(np.float64),
+                                 Lg.cpu().numpy().astype(np.float64), qo, Lo, f"time update {it}")
+        ob = ids[obs]
+        if ob.size:
+            emb, off, pref = W.make_step_inputs(ob.size, d, dtype, prefill_frac=0.0, seed=40 + it)
+            qg, Lg2 = gpu_predict(t, emb, off, ob, pref)
+            qo, Lo = oracle_predict(o, emb, off, ob, pref, dtype)
+            assert_predict_close(qg, Lg2, qo, Lo, f"observation {it}")
+        st = gpu_state(t, ids)
+        np.testing.assert_array_equal(st["age"], o.state.age[ids])
+    # unobserved slots: prior and E_pi[L]; no state change
+    extra = np.arange(n, n + 4, dtype=np.uint32)
+    post = torch.empty((4, k), dtype=torch.float32, device="cuda")
+    Lg = torch.empty(4, dtype=torch.float32, device="cuda")
+    trail_time_update(t.h, dev(extra), 4, 3, post, Lg)
+    torch.cuda.synchronize()
+    qo, Lo = o.time_update(extra, 3)
+    assert np.abs(post.cpu().numpy() - qo).max() <= 1e-6
+    assert np.abs(Lg.cpu().numpy() - Lo).max() <= 1e-3 * Lo.max()
+    assert not gpu_state(t, extra)["seen"].any()
+    t.close()
