@@ -239,6 +239,14 @@ TRAIL_API trail_status trail_trace_read(trail_handle h, uint64_t *host_out, int3
 /* Overrides cfg.l1_mode for subsequent calls (the tcgen05 modes require bf16). */
 TRAIL_API trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode);
 
+/* Preemption-threshold rule (row a4).  0 (default): the paper's static rule, preemptible
+ * while a < floor(c r) with r the initial prediction (D-9, D-10).  1: the dynamic
+ * variant of SURVEY §8(f)3 (reading D-26): preemptible while a < c (a + L_t), i.e. forced
+ * once a >= c L_t / (1 - c) (never for c >= 1), re-evaluated whenever L_t changes
+ * (predict step or time update) and stored as the slot threshold.  Synchronising; CUDA
+ * graphs captured earlier keep the old rule.  Errors: TRAIL_ERR_INVALID (mode not 0/1). */
+TRAIL_API trail_status trail_set_threshold_mode(trail_handle h, int32_t mode);
+
 /* Optional host-side hint: the number of embedding rows (the flat batch's token count,
  * row_offsets[n] - row_offsets[0]) of the next trail_predict_step calls; 0 = unknown (the
  * default).  It only selects the pooling kernel variant and grid (bulk-copy streaming for

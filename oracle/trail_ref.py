@@ -195,6 +195,7 @@ class TrailOracle:
                       else np.asarray(prior, dtype=np.float64))
         self.prior_L = prior_mean_length(self.edges, self.prior)
         self.x_dtype = x_dtype
+        self.threshold = "static"      # or "dynamic" (reading D-26)
         self.state = OracleState(max_slots, self.k)
 
     # ------------------------------------------------------------------ predict
@@ -259,11 +260,17 @@ class TrailOracle:
     # ------------------------------------------------------------------ schedule
     def keys_and_forced(self, ids, is_running) -> Tuple[np.ndarray, np.ndarray]:
         """key = L_t of the slot (E_pi[L] if never observed); forced (rank -inf, P:394,
-        P:830-831) iff running, observed, and age >= floor(c r)."""
+        P:830-831) iff running, observed, and age >= floor(c r) — or, with
+        threshold='dynamic' (reading D-26), age >= c (age + L_t)."""
         ids = np.asarray(ids, dtype=np.int64)
         st = self.state
         key = np.where(st.seen[ids], st.L[ids], self.prior_L)
-        forced = (np.asarray(is_running) != 0) & st.seen[ids] & (st.age[ids] >= st.thr[ids])
+        if self.threshold == "dynamic":
+            a = st.age[ids].astype(np.float64)
+            frozen = a >= self.c * (a + st.L[ids]) if not math.isinf(self.c) else np.zeros(ids.shape, bool)
+        else:
+            frozen = st.age[ids] >= st.thr[ids]
+        forced = (np.asarray(is_running) != 0) & st.seen[ids] & frozen
         return key, forced
 
     def schedule_step(self, ids, arrival_seq, kv_blocks, is_running, kv_budget: int,

@@ -34,7 +34,8 @@ __device__ __forceinline__ float seg_sum(float v, int seg) {
 // Five segment reductions: max z, sum exp, (max, argmax) of the unnormalised log q, sum exp,
 // sum q m.  The D-5 fallback (all-zero product) needs max log p = max z - lse: no reduction.
 __device__ __forceinline__ void head_seg(int j, int n, int k, int SEG, int b, float z,
-                                         const HeadSmem &hc, uint32_t sl, const SlotMeta &mt,
+                                         const HeadSmem &hc, float hc_dyn_c, uint32_t sl,
+                                         const SlotMeta &mt,
                                          float lq_prev, const float *__restrict__ prior_override,
                                          float *__restrict__ lq_state, SlotMeta *__restrict__ meta,
                                          float *__restrict__ post, float *__restrict__ Lout,
@@ -101,6 +102,7 @@ __device__ __forceinline__ void head_seg(int j, int n, int k, int SEG, int b, fl
       o.age += 1;
     }
     o.L = L;
+    if (hc_dyn_c >= 0.f) o.thr = dynamic_threshold(hc_dyn_c, L);
     meta[slot] = o;
     if (Lout) Lout[j] = L;
   }

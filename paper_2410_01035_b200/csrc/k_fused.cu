@@ -392,7 +392,7 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
         for (int t = 0; t < NT; ++t) z += __ldcg(zpart + ((int64_t)j * NT + t) * k + b);
       }
       const int rr = rv ? r : 0;
-      head_seg(j, n, k, SEG, b, z, hc, rv ? s_slot[r] : 0xFFFFFFFFu, s_meta[rr],
+      head_seg(j, n, k, SEG, b, z, hc, cst.dyn_c, rv ? s_slot[r] : 0xFFFFFFFFu, s_meta[rr],
                b < KB ? s_lq[rr * KB + (b < KB ? b : 0)] : -INFINITY, prior_override, lq_state,
                meta, post, Lout, err);
     }

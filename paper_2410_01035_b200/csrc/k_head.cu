@@ -154,6 +154,7 @@ trail_head_kernel(const float *__restrict__ partial, int splits, int n,
       mt.age += 1;
     }
     mt.L = L;
+    if (cst->dyn_c >= 0.f) mt.thr = dynamic_threshold(cst->dyn_c, L);
     if (active) {
       lq_state[(int64_t)slot * k + lane] = lq;
       if (post) post[(int64_t)j * k + lane] = q;

@@ -61,6 +61,7 @@ trail_time_update_kernel(const uint32_t *__restrict__ ids, int n, int steps,
   if (lane == 0) {
     mt.age += (uint32_t)steps;
     mt.L = L;
+    if (cst->dyn_c >= 0.f) mt.thr = dynamic_threshold(cst->dyn_c, L);
     meta[slot] = mt;
     if (Lout) Lout[j] = L;
   }

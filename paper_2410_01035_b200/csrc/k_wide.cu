@@ -250,7 +250,7 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
       float z = 0.f;
       if (j < n && b < k)
         z = (__ldg(b2 + b) + zs[rr * KBP + b]) + zs[(WBM + rr) * KBP + b];
-      head_seg(j, n, k, SEG, b, z, hs, j < n ? s_slot[rr] : 0xFFFFFFFFu, s_meta[rr],
+      head_seg(j, n, k, SEG, b, z, hs, cst.dyn_c, j < n ? s_slot[rr] : 0xFFFFFFFFu, s_meta[rr],
                b < KB ? s_lq[rr * KB + (b < KB ? b : 0)] : -INFINITY, prior_override, lq_state,
                meta, post, Lout, err);
     }

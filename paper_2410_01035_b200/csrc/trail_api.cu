@@ -280,6 +280,7 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
     }
   }
   hc.prior_L = (float)prior_L;
+  hc.dyn_c = -1.f;            // static threshold floor(c r) unless trail_set_threshold_mode
 
   // ---- device memory
   const size_t w1_bytes = (size_t)c.H * c.d * c.esize;
@@ -383,6 +384,17 @@ trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode) {
   if (!h || l1_mode < 0 || l1_mode > 4) return TRAIL_ERR_INVALID;
   if (l1_mode >= TRAIL_L1_UMMA && h->c.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
   h->c.cfg.l1_mode = l1_mode;
+  return TRAIL_OK;
+}
+
+trail_status trail_set_threshold_mode(trail_handle h, int32_t mode) {
+  if (!h || mode < 0 || mode > 1) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  c.host_consts.dyn_c = mode == 1 ? (float)std::min(c.cfg.c, 1e30) : -1.f;
+  if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  if (cudaDeviceSynchronize() != cudaSuccess ||
+      cudaMemcpy(c.consts, &c.host_consts, sizeof(HeadConsts), cudaMemcpyHostToDevice) != cudaSuccess)
+    return TRAIL_ERR_CUDA;
   return TRAIL_OK;
 }
 

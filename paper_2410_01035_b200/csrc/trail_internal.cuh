@@ -41,7 +41,18 @@ struct HeadConsts {
   float prior_L;            // E_pi[L] (D-24)
   int k;
   int H;
+  float dyn_c;              // < 0: static threshold floor(c r); else the dynamic
+                            // variant: forced iff a >= c (a + L_t)
 };
+
+// Dynamic-threshold variant: the smallest integer age a with a >= c (a + L), i.e.
+// a >= c L / (1 - c) for c < 1 (never for c >= 1), recomputed whenever L changes and stored
+// as the slot threshold, so every selection kernel keeps testing a >= thr.
+__host__ __device__ __forceinline__ uint32_t dynamic_threshold(float c, float L) {
+  if (!(c < 1.f)) return 0xFFFFFFFFu;
+  const float t = ceilf(c * L / (1.f - c));
+  return t >= 4294967040.f ? 0xFFFFFFFEu : (t <= 0.f ? 0u : (uint32_t)t);
+}
 
 struct Ctx {
   trail_config cfg;

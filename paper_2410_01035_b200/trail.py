@@ -81,6 +81,7 @@ _SIGS = {
     "trail_set_l1_mode": ([_P, _I32], _I32),
     "trail_set_rows_hint": ([_P, _I64], _I32),
     "trail_time_update": ([_P, _P, _I32, _I32, _P, _P, _P], _I32),
+    "trail_set_threshold_mode": ([_P, _I32], _I32),
     "trail_trace_enable": ([_P, _I32], _I32),
     "trail_trace_read": ([_P, _P, _I32], _I32),
     "trail_plan_l1": ([_P, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)], _I32),
@@ -243,6 +244,10 @@ def trail_time_update(h, request_ids, n: int, steps: int, posteriors, expected_r
     _check("trail_time_update", _lib().trail_time_update(
         h, _ptr(request_ids), int(n), int(steps), _ptr(posteriors), _ptr(expected_remaining),
         _stream(stream)))
+
+
+def trail_set_threshold_mode(h, mode: int) -> None:
+    _check("trail_set_threshold_mode", _lib().trail_set_threshold_mode(h, int(mode)))
 
 
 def trail_set_rows_hint(h, rows: int) -> None:

@@ -106,6 +106,7 @@ def test_null_handle_calls_are_invalid(lib):
                                    None) == -1
     assert lib.trail_time_update(None, None, 1, 1, None, None, None) == -1
     assert lib.trail_set_rows_hint(None, 0) == -1
+    assert lib.trail_set_threshold_mode(None, 1) == -1
     assert lib.trail_destroy(None) == -1
 
 

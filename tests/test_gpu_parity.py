@@ -461,3 +461,52 @@ def test_time_update_predict_every_k(dtype, n, d, k):
     assert np.abs(Lg.cpu().numpy() - Lo).max() <= 1e-3 * Lo.max()
     assert not gpu_state(t, extra)["seen"].any()
     t.close()
+
+
+@pytest.mark.parametrize("c,l1", [(0.5, 0), (0.25, 4), (0.3, 1)])
+def test_dynamic_threshold_mode(c, l1):
+    """Dynamic-threshold variant (trail_set_threshold_mode 1, reading D-26): forced iff
+    a >= c (a + L_t), re-evaluated by every kernel that refreshes L_t (head, fused, wide,
+    time update).  Forced flags match the oracle except within the fp32 band of the
+    boundary; the selection is bit-exact on the GPU's own keys and flags."""
+    from paper_2410_01035_b200.trail import trail_set_threshold_mode
+    n, d, k = 300, 1024, 10
+    w = W.make_weights(d, 512, k, "bf16", seed=51)
+    t, o = make_pair(w, c, n, n, n, "bf16", l1_mode=l1)
+    trail_set_threshold_mode(t.h, 1)
+    o.threshold = "dynamic"
+    ids = np.arange(n, dtype=np.uint32)
+    emb, off, pref = W.make_step_inputs(n, d, "bf16", prefill_frac=1.0, seed=52)
+    gpu_predict(t, emb, off, ids, pref)
+    oracle_predict(o, emb, off, ids, pref, "bf16")
+    rs = np.random.default_rng(53)
+    running = (rs.random(n) < 0.85).astype(np.uint8)
+    arrival = rs.permutation(n).astype(np.uint32)
+    kv = rs.integers(1, 40, n).astype(np.int32)
+    n_forced = 0
+    for it in range(40):
+        if it % 3 == 2:
+            t.time_update(dev(ids), 5)
+            torch.cuda.synchronize()
+            o.time_update(ids, 5)
+        else:
+            emb, off, pref = W.make_step_inputs(n, d, "bf16", prefill_frac=0.0, seed=60 + it)
+            gpu_predict(t, emb, off, ids, pref)
+            oracle_predict(o, emb, off, ids, pref, "bf16")
+        key, forced, st = gpu_keys_forced(t, ids, running, o.prior_L)
+        _, fo = o.keys_and_forced(ids, running)
+        a, L = o.state.age[ids].astype(np.float64), o.state.L[ids]
+        near = np.abs(a * (1 - c) - c * L) <= 4e-3 * c * L + 1e-6
+        assert np.all((forced == fo) | near), it
+        n_forced += int(forced.sum())
+        run, pre, adm, cnt = t.schedule(dev(ids), dev(arrival), dev(kv), dev(running),
+                                        int(0.6 * kv.sum()))
+        torch.cuda.synchronize()
+        cc = cnt.cpu().numpy()
+        r_o, p_o, a_o, s_o = R.select(key, forced, arrival, kv, running, ids.astype(np.int64),
+                                      int(0.6 * kv.sum()), 0)
+        np.testing.assert_array_equal(run[:cc[0]].cpu().numpy(), r_o)
+        np.testing.assert_array_equal(pre[:cc[1]].cpu().numpy(), p_o)
+        assert cc[3] == s_o
+    assert n_forced > 0
+    t.close()

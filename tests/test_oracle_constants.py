@@ -293,3 +293,33 @@ def test_time_update_closed_form_matrix_power_and_state():
     assert np.all(o.state.age[:4] == 3) and o.state.age[6] == 0 and not o.state.seen[6]
     np.testing.assert_allclose(qt[4], np.full(10, 0.1))
     assert Lt[4] == pytest.approx(256.0)
+
+
+def test_dynamic_threshold_special_cases():
+    """Dynamic-threshold variant (reading D-26): forced iff a >= c (a + L).
+    c = 0 freezes every observed running request (the static rule's c = 0 case, D-13);
+    c >= 1 never freezes (full SPRPT, like c = inf, D-14); for 0 < c < 1 the boundary is
+    a = c L / (1 - c), and with L falling one unit per iteration (T only) a frozen request
+    stays frozen."""
+    w_ = W.make_weights(64, 128, 10, "f32", seed=5)
+    emb, off, pref = W.make_step_inputs(16, 64, "f32", prefill_frac=1.0, seed=6)
+    run = np.ones(16, np.uint8)
+    out = {}
+    for c in (0.0, 0.5, 1.0, 3.0):
+        o = R.TrailOracle(w_["W1"], w_["b1"], w_["W2"], w_["b2"], w_["edges"], c, 16, x_dtype="f32")
+        o.threshold = "dynamic"
+        o.predict_step(W.decode(emb, "f32"), off, np.arange(16), pref)
+        hist = []
+        for _ in range(400):
+            o.time_update(np.arange(16), 1)
+            _, f = o.keys_and_forced(np.arange(16), run)
+            a, L = o.state.age[:16].astype(float), o.state.L[:16]
+            if 0 < c < 1:
+                np.testing.assert_array_equal(f, a >= c * L / (1 - c) - 1e-9 * L)
+            hist.append(f)
+        hist = np.array(hist)
+        assert np.all(hist[1:] >= hist[:-1])          # once frozen, stays frozen
+        out[c] = hist
+    assert out[0.0].all()
+    assert not out[1.0].any() and not out[3.0].any()
+    assert out[0.5][0].sum() == 0 and out[0.5][-1].sum() == 16
