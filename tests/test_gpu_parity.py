@@ -510,3 +510,29 @@ def test_dynamic_threshold_mode(c, l1):
         assert cc[3] == s_o
     assert n_forced > 0
     t.close()
+
+
+@pytest.mark.parametrize("l1", [1, 2, 4])
+def test_log_spaced_bins(l1):
+    """Log-spaced bins: unequal widths w_i give a non-uniform T
+    (T_ii = 1 - 1/w_i, T_i,i+1 = 1/w_{i+1}); every layer-1 kernel + head path follows the
+    oracle over a prefill and 30 decode steps with time updates in between."""
+    edges = np.array([0.0, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048])
+    k, n, d = edges.size - 1, 96, 1024
+    w = W.make_weights(d, 512, k, "bf16", edges=edges, seed=71)
+    t, o = make_pair(w, 0.5, n, n, n, "bf16", l1_mode=l1)
+    ids = np.arange(n, dtype=np.uint32)
+    for step in range(31):
+        emb, off, pref = W.make_step_inputs(n, d, "bf16", prefill_frac=1.0 if step == 0 else 0.0,
+                                            seed=72, step=step)
+        qg, Lg = gpu_predict(t, emb, off, ids, pref)
+        qo, Lo = oracle_predict(o, emb, off, ids, pref, "bf16")
+        assert_predict_close(qg, Lg, qo, Lo, f"step {step}")
+        if step % 10 == 9:
+            post, L = t.time_update(dev(ids), 3)
+            torch.cuda.synchronize()
+            qo, Lo = o.time_update(ids, 3)
+            assert_predict_close(post.cpu().numpy().astype(np.float64),
+                                 L.cpu().numpy().astype(np.float64), qo, Lo, f"time update {step}")
+    np.testing.assert_array_equal(gpu_state(t, ids)["age"], o.state.age[ids])
+    t.close()
