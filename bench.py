@@ -428,51 +428,67 @@ def run_ours(args, cfg):
 def run_e2e(args, cfg, t, batches, stream, flush, torch, device, world):
     """Same metric through the public API with pinned HOST inputs/outputs: per step the H2D
     copy of that step's inputs, predict + schedule, and the D2H read of posteriors, expected
-    lengths, counts and the three lists, all inside the per-step CUDA-event bracket."""
+    lengths, counts and the three lists, all inside the per-step CUDA-event bracket.  The
+    step's inputs live in ONE pinned host buffer (16-byte aligned fields) and travel in one
+    copy; the outputs are views of ONE device buffer read back in one copy (the API takes
+    plain pointers, so the caller chooses the layout)."""
     nb = len(batches)
+    names = ("emb", "off", "ids", "pref", "sids", "arr", "kv", "run")
+
+    def al(x):
+        return (x + 15) & ~15
+
     host = []
     for b in batches:
-        h = {}
-        for name, arr in (("emb", b.emb), ("off", b.row_offsets), ("ids", b.request_ids),
-                          ("pref", b.is_prefill), ("sids", b.sched_ids), ("arr", b.arrival_seq),
-                          ("kv", b.kv_blocks), ("run", b.is_running)):
+        arrs = {}
+        for name, arr in zip(names, (b.emb, b.row_offsets, b.request_ids, b.is_prefill,
+                                     b.sched_ids, b.arrival_seq, b.kv_blocks, b.is_running)):
             a = np.ascontiguousarray(arr)
             if a.dtype == np.uint32:
                 a = a.view(np.int32)
-            h[name] = torch.from_numpy(a).pin_memory()
-        h["budget"], h["n"], h["m"] = b.kv_budget, b.n, b.m
+            arrs[name] = a
+        offs, tot = {}, 0
+        for name in names:
+            offs[name] = tot
+            tot = al(tot + arrs[name].nbytes)
+        buf = torch.empty(tot, dtype=torch.uint8).pin_memory()
+        bn = buf.numpy()
+        for name in names:
+            bn[offs[name]:offs[name] + arrs[name].nbytes] = arrs[name].view(np.uint8).reshape(-1)
+        h = {"buf": buf, "bytes": tot, "offs": offs,
+             "meta": {nm: (arrs[nm].dtype, arrs[nm].shape) for nm in names},
+             "budget": b.kv_budget, "n": b.n, "m": b.m}
         host.append(h)
-    dbuf = {k: torch.empty(max(v.numel() for v in (hh[k] for hh in host)), dtype=host[0][k].dtype,
-                           device=device) for k in host[0] if isinstance(host[0][k], torch.Tensor)}
-    cap = t.run_ids.numel()
-    out_host = {"post": torch.empty_like(t.post, device="cpu").pin_memory(),
-                "L": torch.empty_like(t.L, device="cpu").pin_memory(),
-                "counts": torch.empty(4, dtype=torch.int32).pin_memory(),
-                "lists": torch.empty(3 * cap, dtype=torch.int32).pin_memory()}
-    lists_dev = torch.empty(3 * cap, dtype=torch.int32, device=device)
+    dbuf = torch.empty(max(h["bytes"] for h in host), dtype=torch.uint8, device=device)
+    tdt = {np.dtype(np.uint16): torch.uint16, np.dtype(np.float32): torch.float32,
+           np.dtype(np.int32): torch.int32, np.dtype(np.uint8): torch.uint8}
+    # outputs: one device arena, the handle's output pointers are views of it
+    k, cap, R = cfg["k"], t.run_ids.numel(), t.post.shape[0]
+    osz = [al(R * k * 4), al(R * 4), 16, al(cap * 4), al(cap * 4), al(cap * 4)]
+    oarena = torch.zeros(sum(osz), dtype=torch.uint8, device=device)
+    o = np.cumsum([0] + osz)
+    t.post = oarena[o[0]:o[0] + R * k * 4].view(torch.float32).view(R, k)
+    t.L = oarena[o[1]:o[1] + R * 4].view(torch.float32)
+    t.counts = oarena[o[2]:o[2] + 16].view(torch.int32)
+    t.run_ids = oarena[o[3]:o[3] + cap * 4].view(torch.int32)
+    t.preempt_ids = oarena[o[4]:o[4] + cap * 4].view(torch.int32)
+    t.admit_ids = oarena[o[5]:o[5] + cap * 4].view(torch.int32)
+    out_host = torch.empty(oarena.numel(), dtype=torch.uint8).pin_memory()
 
     def step(i):
         h = host[i % nb]
-        n, m = h["n"], h["m"]
+        dv = dbuf[: h["bytes"]]
+        dv.copy_(h["buf"], non_blocking=True)
         views = {}
-        for k, v in h.items():
-            if isinstance(v, torch.Tensor):
-                dv = dbuf[k][: v.numel()]
-                dv.copy_(v.reshape(-1), non_blocking=True)
-                views[k] = dv.view(v.shape)
+        for nm in names:
+            dt, shp = h["meta"][nm]
+            nbytes = int(np.prod(shp)) * np.dtype(dt).itemsize
+            views[nm] = dv[h["offs"][nm]:h["offs"][nm] + nbytes].view(tdt[np.dtype(dt)]).view(shp)
         t.predict(views["emb"], views["off"], views["ids"], views["pref"], stream=stream)
         t.schedule(views["sids"], views["arr"], views["kv"], views["run"], h["budget"],
                    stream=stream)
-        lists_dev[:cap].copy_(t.run_ids)
-        lists_dev[cap:2 * cap].copy_(t.preempt_ids)
-        lists_dev[2 * cap:].copy_(t.admit_ids)
-        out_host["post"][:n].copy_(t.post[:n], non_blocking=True)
-        out_host["L"][:n].copy_(t.L[:n], non_blocking=True)
-        out_host["counts"].copy_(t.counts, non_blocking=True)
-        out_host["lists"].copy_(lists_dev, non_blocking=True)
-        h2d = sum(v.numel() * v.element_size() for v in h.values() if isinstance(v, torch.Tensor))
-        d2h = n * cfg["k"] * 4 + n * 4 + 16 + 3 * cap * 4
-        return h2d, d2h
+        out_host.copy_(oarena, non_blocking=True)
+        return h["bytes"], oarena.numel()
 
     with torch.cuda.stream(stream):
         for i in range(args.warmup):
