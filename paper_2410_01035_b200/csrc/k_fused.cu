@@ -17,9 +17,11 @@
 //   warps 2-7       : stage the W2 / b1 slices of this column tile (overlaps the mainloop)
 //   all 8 warps     : epilogue
 //     1. TMEM -> registers -> own shared memory (fp32 128x128 partial tile, padded rows)
-//     2. cluster barrier; each CTA PUSHES row group r of its tile to CTA r with one bulk
-//        shared::cta -> shared::cluster copy per peer (async engine, completion on the
-//        receiver's mbarrier), so CTA r owns rows [r*128/S, (r+1)*128/S);
+//     2. cluster barrier; CTA r owns rows [r*128/S, (r+1)*128/S) and reads those rows of
+//        every peer's partial tile straight from the peer's shared memory
+//        (ld.shared::cluster, all S loads of an item in flight) — or, with
+//        TRAIL_FUSED_PULL=0, each CTA PUSHES row group r to CTA r with one bulk
+//        shared::cta -> shared::cluster copy per peer (completion on the receiver's mbarrier);
 //     3. CTA r sums its rows over the S partials in fixed rank order (deterministic), adds
 //        b1, ReLU, and contracts its 128 hidden units with W2[:, n0:n0+128] -> z_part;
 //     4. release fence + atomic arrival counter per (m_tile, r); the CTA that completes the
@@ -95,7 +97,8 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
                            const float *__restrict__ prior_override, int max_slots,
                            float *__restrict__ lq_state, SlotMeta *__restrict__ meta,
                            float *__restrict__ post, float *__restrict__ Lout,
-                           uint32_t *__restrict__ err, uint64_t *__restrict__ trace, int spin) {
+                           uint32_t *__restrict__ err, uint64_t *__restrict__ trace, int spin,
+                           int pull) {
   using C = FCfg<KB>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -153,7 +156,7 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // the landing barrier's single arrival, carrying the bytes the S-1 peers will push
-  if (tid == 0 && S > 1) mbar_expect_tx(land, (uint32_t)((S - 1) * rows * ROW_BYTES));
+  if (tid == 0 && S > 1 && !pull) mbar_expect_tx(land, (uint32_t)((S - 1) * rows * ROW_BYTES));
   griddep_launch();
   if (tr && tid == 0) tr[1] = gtimer();
 
@@ -292,7 +295,7 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
 
   // ---- 2. push row group p of my partial tile to CTA p (one bulk copy per peer)
   const uint32_t land_base = smem_u32(smem + LAND_OFF);
-  if (S > 1) {
+  if (S > 1 && !pull) {
     if (tid == 0) {
       for (int q = 1; q < S; ++q) {
         const int p = (crank + q) % S;
@@ -311,7 +314,28 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
   //           (compact loops: these kernels run once per step, so instruction fetch from
   //           L2 is on the critical path and straight-line unrolled code costs more than
   //           it saves)
-  {
+  if (pull && S > 1) {
+    // pull variant: read the peers' partial rows straight from their shared memory
+    // (ld.shared::cluster, all S loads of an item in flight), no landing copies
+    const uint32_t tile_s = smem_u32(tile);
+    for (int i = tid; i < rows * (BN / 4); i += THREADS) {
+      const int r = i >> 5, c = (i & 31) * 4;
+      const uint32_t off = (uint32_t)(((r0 + r) * TILE_LD + c) * 4);
+      float4 v[MAXS];
+#pragma unroll
+      for (int p = 0; p < MAXS; ++p)
+        if (p < S) v[p] = ld_cluster_f4(mapa(tile_s + off, (uint32_t)p));
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int p = 0; p < MAXS; ++p)
+        if (p < S) { acc.x += v[p].x; acc.y += v[p].y; acc.z += v[p].z; acc.w += v[p].w; }
+      const float4 bb = *reinterpret_cast<const float4 *>(b1s + c);
+      *reinterpret_cast<float4 *>(tile + (r0 + r) * TILE_LD + c) =
+          make_float4(fmaxf(acc.x + bb.x, 0.f), fmaxf(acc.y + bb.y, 0.f),
+                      fmaxf(acc.z + bb.z, 0.f), fmaxf(acc.w + bb.w, 0.f));
+    }
+    cluster_arrive();                // done reading the peers (waited on before exit)
+  } else {
     const float *land_f = reinterpret_cast<const float *>(smem + LAND_OFF);
     for (int i = tid; i < rows * (BN / 4); i += THREADS) {
       const int r = i >> 5, c = (i & 31) * 4;
@@ -438,6 +462,16 @@ static cudaError_t fused_occupancy(Ctx &c) {
   return cudaSuccess;
 }
 
+// Split-K reduction by direct DSMEM loads (default; measured 0.9 µs shorter than the bulk
+// push + landing wait at c2); TRAIL_FUSED_PULL=0 selects the push variant for comparison
+static int fused_pull() {
+  static const int v = [] {
+    const char *e = getenv("TRAIL_FUSED_PULL");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v;
+}
+
 static int fused_kb(int k) { return k <= 10 ? 10 : k <= 16 ? 16 : k <= 20 ? 20 : 32; }
 
 cudaError_t fused_prepare(Ctx &c) {
@@ -526,7 +560,7 @@ cudaError_t launch_fused_predict(Ctx &c, const void *emb, int64_t ld, const int3
                             c.d / BK, splits, (const float *)c.b1, (const float *)c.w2,           \
                             (const float *)c.b2, c.host_consts, c.zpart,                                  \
                             c.arrive_cnt, ids, is_prefill, prior_override, c.cfg.max_slots, c.lq, \
-                            c.meta, post, L, c.dev_err, trace, spin)
+                            c.meta, post, L, c.dev_err, trace, spin, fused_pull())
   switch (fused_kb(c.k)) {
     case 10: TRAIL_FUSED(10);
     case 16: TRAIL_FUSED(16);
