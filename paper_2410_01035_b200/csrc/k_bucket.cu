@@ -16,10 +16,8 @@
 //       is staged in shared memory; 8 threads per record), adds the bucket prefixes
 //       -> position, cumulative KV, running-before, and the lists follow as in k_rank.cu
 //       (one packed acq_rel atomic; the last CTA writes the preempt list and re-arms).
-// Cost is O(m + sum over buckets of size^2 / 8) for ordinary ranges; a CTA whose staged
-// bucket range is large (a tie cluster, e.g. never-observed requests all keyed E_pi[L])
-// bitonic-sorts it in shared memory instead and reads positions and prefix sums off the
-// sorted range (O(s log^2 s)).
+// Cost is O(m + sum over buckets of size^2 / 8); a tie cluster (e.g. never-observed requests,
+// all keyed E_pi[L]) is spread over the CTAs that own its positions.
 #include <algorithm>
 
 #include "trail_internal.cuh"
@@ -32,7 +30,6 @@ constexpr int kB = 2 * kBH;
 constexpr int kB3Threads = 1024;
 constexpr int kB3Items = kB3Threads / 8;
 constexpr int kStageCap = 8192;         // bucket entries staged in shared memory (128 KB)
-constexpr int kSortMin = 2048;          // staged ranges at least this long are sorted, not counted
 
 struct BkEntry {                        // bucket-sorted record (16 B)
   unsigned long long key;               // keybits << 32 | arrival
@@ -225,124 +222,18 @@ trail_bucket_rank_kernel(int m, float m0, float scale, uint32_t *__restrict__ hc
   const bool have = p < p1;
   BkEntry me;
   int bs = 0, be = 0, b = 0;
+  if (have) {
+    me = staged ? stage[p - lo] : sorted[p];
+    b = bk_bucket((uint32_t)(me.key >> 32), m0, scale);
+    bs = (int)sh.cnt[b];
+    be = b + 1 < kB ? (int)sh.cnt[b + 1] : nv;
+  }
   uint32_t cnt = 0, rb = 0;
   unsigned long long cum = 0;
-  if (staged && hi - lo >= kSortMin) {
-    // a large staged range (a tie cluster, e.g. never-observed requests all keyed E_pi[L]):
-    // counting would cost size^2; instead bitonic-sort the staged buckets in shared memory
-    // (keys (key, gid) are unique, so every CTA staging this range gets the same order), so
-    // the entry at staged index p - lo IS the record with final position p, and the
-    // within-bucket KV / running counts are prefix sums over the sorted range
-    const int N0 = hi - lo;
-    int N = 1;
-    while (N < N0) N <<= 1;
-    for (int q = N0 + t; q < N; q += kB3Threads) {
-      stage[q].key = ~0ull;
-      stage[q].kv = 0u;
-      stage[q].gid = 0x7FFFFFFFu;
-    }
-    __syncthreads();
-    for (int kk = 2; kk <= N; kk <<= 1)
-      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-        for (int i = t; i < N; i += kB3Threads) {
-          const int l = i ^ jj;
-          if (l > i) {
-            const BkEntry x = stage[i], y = stage[l];
-            const bool up = (i & kk) == 0;
-            if (up ? bk_less(y, x) : bk_less(x, y)) { stage[i] = y; stage[l] = x; }
-          }
-        }
-        __syncthreads();
-      }
-    // inclusive prefix over the sorted range of (kv, running): 8 entries per thread, stored
-    // packed (kv << 24 | running) in the prefix area behind the stage
-    unsigned long long *pref = reinterpret_cast<unsigned long long *>(stage + kStageCap);
-    {
-      constexpr int PER = kStageCap / kB3Threads;   // 8
-      unsigned long long a[PER];
-      uint32_t rr[PER];
-      unsigned long long sa = 0;
-      uint32_t sr = 0;
-#pragma unroll
-      for (int u = 0; u < PER; ++u) {
-        const int q = t * PER + u;
-        const BkEntry e = q < N0 ? stage[q] : BkEntry{0ull, 0u, 0u};
-        sa += e.kv;
-        sr += e.gid >> 31;
-        a[u] = sa;
-        rr[u] = sr;
-      }
-      // exclusive block scan of the per-thread totals (reuse the bucket-scan warp slots)
-      const int lane = t & 31, w = t >> 5;
-      unsigned long long xa = sa;
-      uint32_t xr = sr;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long ya = __shfl_up_sync(0xffffffffu, xa, o);
-        const uint32_t yr = __shfl_up_sync(0xffffffffu, xr, o);
-        if (lane >= o) { xa += ya; xr += yr; }
-      }
-      __shared__ unsigned long long s_wa[32];
-      __shared__ uint32_t s_wr[32];
-      if (lane == 31) { s_wa[w] = xa; s_wr[w] = xr; }
-      __syncthreads();
-      if (w == 0) {
-        unsigned long long va = s_wa[lane];
-        uint32_t vr = s_wr[lane];
-        const unsigned long long va0 = va;
-        const uint32_t vr0 = vr;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned long long ya = __shfl_up_sync(0xffffffffu, va, o);
-          const uint32_t yr = __shfl_up_sync(0xffffffffu, vr, o);
-          if (lane >= o) { va += ya; vr += yr; }
-        }
-        s_wa[lane] = va - va0;
-        s_wr[lane] = vr - vr0;
-      }
-      __syncthreads();
-      const unsigned long long ba = s_wa[w] + xa - sa;
-      const uint32_t br = s_wr[w] + xr - sr;
-      __syncthreads();                                 // every thread read its entries
-      // overwrite each entry's kv / gid-high with its EXCLUSIVE prefix (kv: u64 in key slot
-      // is still needed -> keep the key; store prefix kv in a parallel view of .kv + .gid)
-#pragma unroll
-      for (int u = 0; u < PER; ++u) {
-        const int q = t * PER + u;
-        if (q < N0) {
-          const unsigned long long inc = ba + a[u];
-          const uint32_t incr = br + rr[u];
-          pref[q] = (inc << 24) | incr;
-        }
-      }
-    }
-    __syncthreads();
-    if (have) {
-      me = stage[p - lo];
-      b = bk_bucket((uint32_t)(me.key >> 32), m0, scale);
-      bs = (int)sh.cnt[b];
-      be = b + 1 < kB ? (int)sh.cnt[b + 1] : nv;
-      const unsigned long long mine = pref[p - lo];
-      const unsigned long long first = bs - lo > 0 ? pref[bs - lo - 1] : 0ull;
-      // exclusive within-bucket totals: records of the bucket before me
-      const unsigned long long mine_ex = mine - (((unsigned long long)me.kv << 24) | (me.gid >> 31));
-      cnt = (uint32_t)(p - bs);
-      cum = (mine_ex >> 24) - (first >> 24);
-      rb = (uint32_t)((mine_ex & 0xFFFFFFull) - (first & 0xFFFFFFull));
-    }
-    if (part != 0) { cnt = 0; cum = 0; rb = 0; }   // one thread per record carries the result
-  } else {
-    if (have) {
-      me = staged ? stage[p - lo] : sorted[p];
-      b = bk_bucket((uint32_t)(me.key >> 32), m0, scale);
-      bs = (int)sh.cnt[b];
-      be = b + 1 < kB ? (int)sh.cnt[b + 1] : nv;
-    }
-    if (have) {
-      for (int q = bs + part; q < be; q += 8) {
-        const BkEntry o = staged ? stage[q - lo] : sorted[q];
-        if (bk_less(o, me)) { ++cnt; cum += o.kv; rb += o.gid >> 31; }
-      }
+  if (have) {
+    for (int q = bs + part; q < be; q += 8) {
+      const BkEntry o = staged ? stage[q - lo] : sorted[q];
+      if (bk_less(o, me)) { ++cnt; cum += o.kv; rb += o.gid >> 31; }
     }
   }
 #pragma unroll
@@ -405,7 +296,7 @@ cudaError_t select_bucket_prepare() {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BkScan));
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(trail_bucket_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(sizeof(BkScan) + kStageCap * (sizeof(BkEntry) + 8)));
+                              (int)(sizeof(BkScan) + kStageCap * sizeof(BkEntry)));
 }
 
 cudaError_t launch_select_bucket(const Ctx &c, const Record *rec, int m, int64_t budget,
@@ -434,7 +325,7 @@ cudaError_t launch_select_bucket(const Ctx &c, const Record *rec, int m, int64_t
   if (e != cudaSuccess) return e;
   const int g3 = std::max(1, (m + kB3Items - 1) / kB3Items);
   return launch_k(trail_bucket_rank_kernel, dim3(g3), dim3(kB3Threads),
-                  sizeof(BkScan) + kStageCap * (sizeof(BkEntry) + 8), s, m, m0, scale, hcnt, hrun, hkv,
+                  sizeof(BkScan) + kStageCap * sizeof(BkEntry), s, m, m0, scale, hcnt, hrun, hkv,
                   cursor, (const BkEntry *)sorted, (long long)budget, max_run, gcnt, scratch, run,
                   pre, adm, counts);
 }
