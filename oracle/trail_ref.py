@@ -207,6 +207,25 @@ class TrailOracle:
             X[j] = pool_embedding(emb[row_offsets[j]:row_offsets[j + 1]], self.x_dtype)
         return X
 
+    def prefill_chunk(self, emb: np.ndarray, row_offsets: np.ndarray, request_ids: np.ndarray,
+                      is_final: np.ndarray) -> np.ndarray:
+        """Chunked prefill (P:432 vLLM chunked prefill, reading D-27): the
+        rows of a prompt arrive over several iterations; the pooled input is still the mean
+        of ALL prompt rows.  Accumulates each chunk's rows per slot; for requests
+        whose chunk is the last returns the pooled row (pool_embedding of every row seen),
+        NaN rows otherwise."""
+        if not hasattr(self, "_chunks"):
+            self._chunks = {}
+        ids = np.asarray(request_ids, dtype=np.int64)
+        off = np.asarray(row_offsets, dtype=np.int64)
+        out = np.full((ids.shape[0], emb.shape[1]), np.nan)
+        for j, sid in enumerate(ids):
+            rows = np.asarray(emb[off[j]:off[j + 1]], dtype=np.float64)
+            self._chunks.setdefault(int(sid), []).append(rows)
+            if is_final[j]:
+                out[j] = pool_embedding(np.concatenate(self._chunks.pop(int(sid))), self.x_dtype)
+        return out
+
     def probs(self, X: np.ndarray) -> np.ndarray:
         """p^(t) = softmax(MLP(u^(t))) (a2 + first half of a3)."""
         return softmax(classifier_logits(X, self.W1, self.b1, self.W2, self.b2))

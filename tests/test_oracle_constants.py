@@ -323,3 +323,24 @@ def test_dynamic_threshold_special_cases():
     assert out[0.0].all()
     assert not out[1.0].any() and not out[3.0].any()
     assert out[0.5][0].sum() == 0 and out[0.5][-1].sum() == 16
+
+
+def test_prefill_chunk_oracle_is_the_mean_of_all_rows():
+    """Chunked prefill (D-27): however the prompt is split, the pooled row is the mean of all
+    its rows — pinned against numpy's mean of the unsplit prompt, and a one-chunk
+    prompt against the plain pool."""
+    w_ = W.make_weights(64, 128, 10, "f32", seed=8)
+    o = R.TrailOracle(w_["W1"], w_["b1"], w_["W2"], w_["b2"], w_["edges"], 0.8, 8, x_dtype="f32")
+    rs = np.random.default_rng(9)
+    full = rs.standard_normal((37, 64))
+    cuts = [0, 5, 6, 20, 37]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        out = o.prefill_chunk(full[a:b], np.array([0, b - a]), np.array([3]), np.array([b == 37]))
+    np.testing.assert_allclose(out[0], full.mean(axis=0), rtol=1e-12, atol=1e-15)
+    one = o.prefill_chunk(full, np.array([0, 37]), np.array([4]), np.array([1]))
+    np.testing.assert_allclose(one[0], R.pool_embedding(full, "f32"), rtol=0, atol=0)
+    ob = R.TrailOracle(w_["W1"], w_["b1"], w_["W2"], w_["b2"], w_["edges"], 0.8, 8, x_dtype="bf16")
+    xb = W.decode(W.encode(full.astype(np.float32), "bf16"), "bf16")
+    ob.prefill_chunk(xb[:10], np.array([0, 10]), np.array([1]), np.array([0]))
+    out = ob.prefill_chunk(xb[10:], np.array([0, 27]), np.array([1]), np.array([1]))
+    np.testing.assert_array_equal(out[0], R.bf16_round(xb.mean(axis=0)))
