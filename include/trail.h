@@ -133,6 +133,24 @@ TRAIL_API trail_status trail_predict_step(trail_handle h, const void *emb, int64
                                 int32_t n, float *posteriors, float *expected_remaining,
                                 trail_stream stream);
 
+/* Chunked prefill (P:432 vLLM chunked prefill, reading D-27).  A prompt's
+ * rows may arrive over several iterations; the pooled input is still the mean of ALL its
+ * rows.  For each of the n requests, adds its chunk's rows
+ * [row_offsets[j], row_offsets[j+1]) of emb ([rows][emb_ld], cfg.dtype) to the slot's
+ * running fp32 sum and row count; where is_final[j] != 0 writes the mean of every row
+ * seen — rounded to bf16 (RNE) for bf16 handles, reading D-12 — to row j of `pooled`
+ * ([n][pooled_ld], cfg.dtype, device, caller-owned) and clears the slot's accumulator.
+ * The caller then passes `pooled` rows to trail_predict_step as one-row prefill
+ * observations.  Non-final rows of `pooled` are not written.  Request ids unique within a
+ * call.  The [max_slots][d] fp32 accumulator is allocated on first use (synchronising).
+ * Errors: TRAIL_ERR_INVALID (NULL pointers, ld < d, 16-byte alignment);
+ * TRAIL_DEV_BAD_ID / TRAIL_DEV_BAD_ROWS device bits for bad ids / reversed ranges. */
+TRAIL_API trail_status trail_prefill_chunk(trail_handle h, const void *emb, int64_t emb_ld,
+                                           const int32_t *row_offsets,
+                                           const uint32_t *request_ids, const uint8_t *is_final,
+                                           int32_t n, void *pooled, int64_t pooled_ld,
+                                           trail_stream stream);
+
 /* Iterations without an observation — the "predict every K iterations" variant (P:717,
  * SURVEY §8(f)3).  For each listed slot that has been observed: the transition alone acts,
  * q <- normalise(T q) (readings D-1/D-4, log domain D-22), `steps` times; the

@@ -147,7 +147,8 @@ trail_status set_device(const Ctx &c) {
 void free_ctx(Ctx &c) {
   void *ptrs[] = {c.w1, c.b1, c.w2, c.b2, c.consts, c.lq, c.meta, c.dev_err, c.xs,
                   c.partial, c.rec_local, c.rec_all, c.sel_scratch, c.zpart, c.arrive_cnt, c.trace,
-                  c.rank_sorted, c.rank_cnt, c.pool_head, c.pool_tail, c.pool_cnt, c.bk_ws};
+                  c.rank_sorted, c.rank_cnt, c.pool_head, c.pool_tail, c.pool_cnt, c.bk_ws,
+                  c.chunk_acc, c.chunk_cnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c.prof_ev) {
@@ -462,6 +463,24 @@ trail_status trail_predict_step(trail_handle h, const void *emb, int64_t emb_ld,
     TRAIL_CUDA(launch_head(c, n, splits, request_ids, is_prefill, prior_override, posteriors,
                            expected_remaining, s));
   }
+  return TRAIL_OK;
+}
+
+trail_status trail_prefill_chunk(trail_handle h, const void *emb, int64_t emb_ld,
+                                 const int32_t *row_offsets, const uint32_t *request_ids,
+                                 const uint8_t *is_final, int32_t n, void *pooled,
+                                 int64_t pooled_ld, trail_stream stream) {
+  if (!h || n < 0) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (n == 0) return TRAIL_OK;
+  if (!emb || !row_offsets || !request_ids || !is_final || !pooled) return TRAIL_ERR_INVALID;
+  if (emb_ld < c.d || pooled_ld < c.d || (emb_ld * (int64_t)c.esize) % 16 != 0 ||
+      (pooled_ld * (int64_t)c.esize) % 16 != 0 || ((uintptr_t)emb) % 16 != 0 ||
+      ((uintptr_t)pooled) % 16 != 0)
+    return TRAIL_ERR_INVALID;
+  if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  TRAIL_CUDA(launch_prefill_chunk(c, emb, emb_ld, row_offsets, request_ids, is_final, n, pooled,
+                                  pooled_ld, (cudaStream_t)stream));
   return TRAIL_OK;
 }
 

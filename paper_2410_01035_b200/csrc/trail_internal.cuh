@@ -77,6 +77,8 @@ struct Ctx {
   uint64_t *trace = nullptr;   // diagnostics: per-CTA phase timestamps (trail_trace_enable)
   int trace_cap = 0;           // CTAs the trace buffer holds (16 u64 each)
   int fused_max_clusters[17] = {};
+  float *chunk_acc = nullptr;       // [max_slots][d] chunked-prefill running sums (lazy)
+  uint32_t *chunk_cnt = nullptr;    // [max_slots] rows accumulated so far
   float *pool_head = nullptr;       // [pool_grid][d] K1 partial sums (request began earlier)
   float *pool_tail = nullptr;       // [pool_grid][d] K1 partial sums (request continues)
   uint32_t *pool_cnt = nullptr;     // [max_requests] K1 per-request chunk arrival counters
@@ -139,6 +141,9 @@ cudaError_t launch_select(const Ctx &c, const Record *rec, int n, int64_t budget
                           cudaStream_t s);
 cudaError_t launch_time_update(const Ctx &c, const uint32_t *ids, int n, int steps, float *post,
                                float *L, cudaStream_t s);
+cudaError_t launch_prefill_chunk(Ctx &c, const void *emb, int64_t ld, const int32_t *off,
+                                 const uint32_t *ids, const uint8_t *is_final, int n,
+                                 void *pooled, int64_t pld, cudaStream_t s);
 cudaError_t launch_release(const Ctx &c, const uint32_t *ids, int n, cudaStream_t s);
 cudaError_t launch_read_state(const Ctx &c, const uint32_t *ids, int n, float *L, uint32_t *age,
                               uint32_t *thr, uint8_t *seen, float *post, cudaStream_t s);

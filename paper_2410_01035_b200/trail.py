@@ -81,6 +81,7 @@ _SIGS = {
     "trail_set_l1_mode": ([_P, _I32], _I32),
     "trail_set_rows_hint": ([_P, _I64], _I32),
     "trail_time_update": ([_P, _P, _I32, _I32, _P, _P, _P], _I32),
+    "trail_prefill_chunk": ([_P, _P, _I64, _P, _P, _P, _I32, _P, _I64, _P], _I32),
     "trail_set_threshold_mode": ([_P, _I32], _I32),
     "trail_trace_enable": ([_P, _I32], _I32),
     "trail_trace_read": ([_P, _P, _I32], _I32),
@@ -244,6 +245,13 @@ def trail_time_update(h, request_ids, n: int, steps: int, posteriors, expected_r
     _check("trail_time_update", _lib().trail_time_update(
         h, _ptr(request_ids), int(n), int(steps), _ptr(posteriors), _ptr(expected_remaining),
         _stream(stream)))
+
+
+def trail_prefill_chunk(h, emb, emb_ld: int, row_offsets, request_ids, is_final, n: int,
+                        pooled, pooled_ld: int, stream=None) -> None:
+    _check("trail_prefill_chunk", _lib().trail_prefill_chunk(
+        h, _ptr(emb), int(emb_ld), _ptr(row_offsets), _ptr(request_ids), _ptr(is_final), int(n),
+        _ptr(pooled), int(pooled_ld), _stream(stream)))
 
 
 def trail_set_threshold_mode(h, mode: int) -> None:

@@ -107,6 +107,7 @@ def test_null_handle_calls_are_invalid(lib):
     assert lib.trail_time_update(None, None, 1, 1, None, None, None) == -1
     assert lib.trail_set_rows_hint(None, 0) == -1
     assert lib.trail_set_threshold_mode(None, 1) == -1
+    assert lib.trail_prefill_chunk(None, None, 0, None, None, None, 1, None, 0, None) == -1
     assert lib.trail_destroy(None) == -1
 
 

@@ -536,3 +536,64 @@ def test_log_spaced_bins(l1):
                                  L.cpu().numpy().astype(np.float64), qo, Lo, f"time update {step}")
     np.testing.assert_array_equal(gpu_state(t, ids)["age"], o.state.age[ids])
     t.close()
+
+
+@pytest.mark.parametrize("dtype,d,l1", [("bf16", 4096, 0), ("f32", 1024, 0), ("bf16", 1024, 4)])
+def test_chunked_prefill(dtype, d, l1):
+    """Chunked prefill (trail_prefill_chunk, reading D-27): prompts split into 1-4 chunks over
+    successive calls, interleaved across requests; the finalised pooled rows equal the mean
+    of all prompt rows (within one bf16 ulp / fp32 rounding of the oracle's fp64 mean) and
+    the prediction made from them matches the oracle."""
+    from paper_2410_01035_b200.trail import trail_prefill_chunk
+    n, k = 60, 10
+    w = W.make_weights(d, 512, k, dtype, seed=81)
+    t, o = make_pair(w, 0.8, n, n, n, dtype, l1_mode=l1)
+    rs = np.random.default_rng(82)
+    plen = rs.integers(1, 200, n)
+    nchunks = rs.integers(1, 5, n)
+    full = [W.make_step_inputs(1, d, dtype, prefill_frac=1.0, mean_prompt=int(plen[j]),
+                               seed=83 + j)[0] for j in range(n)]
+    cuts = [np.unique(np.concatenate([[0, plen[j]], rs.integers(1, max(2, plen[j]), nchunks[j] - 1)]))
+            for j in range(n)]
+    pooled_all = np.zeros((n, d), dtype=full[0].dtype)
+    ref_all = np.zeros((n, d))
+    rnd = 0
+    pending = set(range(n))
+    while pending:
+        js = sorted(j for j in pending if rnd < len(cuts[j]) - 1)
+        if not js:
+            break
+        rows, off, fin = [], [0], []
+        for j in js:
+            a, b = cuts[j][rnd], cuts[j][rnd + 1]
+            rows.append(full[j][a:b])
+            off.append(off[-1] + (b - a))
+            fin.append(1 if rnd + 2 == len(cuts[j]) else 0)
+        emb = np.concatenate(rows)
+        off, fin = np.array(off, np.int32), np.array(fin, np.uint8)
+        ids = np.array(js, np.uint32)
+        pooled = torch.empty((len(js), d), dtype=torch.uint16 if dtype == "bf16" else torch.float32,
+                             device="cuda")
+        trail_prefill_chunk(t.h, dev(emb), d, dev(off), dev(ids), dev(fin), len(js), pooled, d)
+        torch.cuda.synchronize()
+        ref = o.prefill_chunk(W.decode(emb, dtype), off, ids, fin)
+        pg = pooled.cpu().numpy()
+        for q, j in enumerate(js):
+            if fin[q]:
+                pooled_all[j] = pg[q].view(pooled_all.dtype) if dtype == "bf16" else pg[q]
+                ref_all[j] = ref[q]
+                pending.discard(j)
+        rnd += 1
+    assert not pending
+    got = W.decode(pooled_all, dtype)
+    tol = np.abs(ref_all) * (2.0 ** -7 if dtype == "bf16" else 1e-5) + 1e-6
+    assert np.all(np.abs(got - ref_all) <= tol)
+    # predict from the pooled rows (one-row prefill observations) vs the oracle on its own
+    ids = np.arange(n, dtype=np.uint32)
+    off1 = np.arange(n + 1, dtype=np.int32)
+    pref = np.ones(n, np.uint8)
+    qg, Lg = gpu_predict(t, pooled_all, off1, ids, pref)
+    ref_store = W.encode(ref_all.astype(np.float32), dtype) if dtype == "bf16" else ref_all.astype(np.float32)
+    qo, Lo = oracle_predict(o, ref_store, off1, ids, pref, dtype)
+    assert_predict_close(qg, Lg, qo, Lo, "chunked prefill")
+    t.close()
