@@ -20,66 +20,74 @@ constexpr int kWarps = 8;
 constexpr int kGemvSmemMax = 200 * 1024;   // W1 + X slices staged in shared memory
 }  // namespace
 
-// Broadcast GEMV (the kernel K2a launches): no cross-lane reduction at all.  A CTA owns 64
-// hidden rows x the K range of its split and stages both operand slices in shared memory with
-// cp.async; lane = request, warp = (request group of 32, 16 rows).  Shared memory is K4-major
-// — [K/4][64 rows][4 elements] for W1 and [K/4][64 requests][4 elements] for X — so for each
-// group of 4 K columns a lane reads its X vector (lanes consecutive: conflict-free) and the 16
-// W1 vectors its warp shares (broadcast) at compile-time offsets from one moving pointer,
-// then issues 64 FFMAs: 17 LDS per 64 FFMA and no address arithmetic in the loop.
-constexpr int kGbRows = 64, kGbReq = 64, kGbRpw = 16;
+// Register-tiled GEMV (the kernel K2a launches).  A CTA owns 64 hidden rows x the K range of
+// its split; both operand slices are staged in shared memory "group-major": [K/G][64][G]
+// with G = 16 B of elements (4 fp32 / 8 bf16) — W1 by TMA (one 64-row x 16-byte box per
+// group, issued by one thread before the PDL wait), X by cp.async (rows from emb or xs).
+// 8 warps = 2 K halves x 4 warp tiles of 32 requests x 32 rows; lane = 4 requests x 8 rows
+// (requests lq, lq+8, lq+16, lq+24 of its tile: the 8 lanes of a quarter-warp read 8
+// consecutive X vectors, conflict-free; its 8 rows are a shared broadcast per quarter-warp).
+// Per group a lane loads 4 X + 8 W1 vectors (12 LDS.128) for 32 G FFMAs — 2.8x fewer
+// shared-memory wavefronts per FFMA than the 1-request-per-lane broadcast form — and the two
+// K halves are added in a fixed order (deterministic).
+constexpr int kGbRows = 64, kGbReq = 64;
 
 template <typename T>
-struct Q4;   // 4 consecutive elements
+struct G16;   // one 16-byte group of elements
 template <>
-struct Q4<float> {
-  using V = uint4;
-  static __device__ __forceinline__ void widen(const V &u, float (&f)[4]) {
+struct G16<float> {
+  static constexpr int G = 4;
+  static __device__ __forceinline__ void widen(const uint4 &u, float (&f)[4]) {
     f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
     f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
   }
 };
 template <>
-struct Q4<__nv_bfloat16> {
-  using V = uint2;
-  static __device__ __forceinline__ void widen(const V &u, float (&f)[4]) {
-    f[0] = __uint_as_float(u.x << 16); f[1] = __uint_as_float(u.x & 0xFFFF0000u);
-    f[2] = __uint_as_float(u.y << 16); f[3] = __uint_as_float(u.y & 0xFFFF0000u);
+struct G16<__nv_bfloat16> {
+  static constexpr int G = 8;
+  static __device__ __forceinline__ void widen(const uint4 &u, float (&f)[8]) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
   }
 };
 
-// copy 4 consecutive elements (16 B fp32 / 8 B bf16) global -> shared, asynchronously
-template <typename T>
-__device__ __forceinline__ void cp4(void *dst, const T *src) {
-  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-  if (sizeof(T) == 4)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-}
-
 template <typename T>
 __global__ void __launch_bounds__(kWarps * 32, 1)
-trail_gemv_l1_kernel(const T *__restrict__ w1, const T *__restrict__ emb, int64_t ld,
-                     const int32_t *__restrict__ off, const T *__restrict__ xs, int n, int d, int H,
-                     int kchunk, float *__restrict__ partial) {
-  using V = typename Q4<T>::V;
-  constexpr int QB = 4 * (int)sizeof(T);                 // bytes of one 4-element group
-  extern __shared__ __align__(16) uint8_t gsm[];
+trail_gemv_l1_kernel(const __grid_constant__ CUtensorMap tmap_w, const T *__restrict__ emb,
+                     int64_t ld, const int32_t *__restrict__ off, const T *__restrict__ xs, int n,
+                     int d, int H, int kchunk, float *__restrict__ partial) {
+  constexpr int G = G16<T>::G;
+  extern __shared__ __align__(128) uint8_t gsm[];
+  __shared__ __align__(8) uint64_t s_bar;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int o0 = blockIdx.x * kGbRows;
   const int s = blockIdx.y;
   const int kb = s * kchunk;
   const int kc = max(0, min(d, kb + kchunk) - kb);
-  const int nq = kc / 4;                                 // 4-element groups of the K range
-  uint8_t *wsm = gsm;                                    // [nq][64][QB]
-  uint8_t *xsm = gsm + (size_t)nq * kGbRows * QB;        // [nq][64][QB]
-  int64_t *src = reinterpret_cast<int64_t *>(xsm + (size_t)nq * kGbReq * QB);   // [64]
-  // W1 slice: a weight, independent of earlier kernels — in flight before the PDL wait
-  for (int r = warp; r < kGbRows; r += kWarps)          // a warp per row: coalesced reads
-    for (int q = lane; q < nq; q += 32)
-      cp4<T>(wsm + ((size_t)q * kGbRows + r) * QB, w1 + (int64_t)(o0 + r) * d + kb + 4 * q);
-  asm volatile("cp.async.commit_group;" ::: "memory");
+  const int ng = kc / G;                                 // 16-byte groups of the K range
+  uint8_t *wsm = gsm;                                    // [ng][64 rows][16 B]
+  uint8_t *xsm = gsm + (size_t)ng * kGbRows * 16;        // [ng][64 requests][16 B]
+  int64_t *src = reinterpret_cast<int64_t *>(xsm + (size_t)ng * kGbReq * 16);   // [64]
+  float *red = reinterpret_cast<float *>(src + kGbReq);  // [4 tiles][32 acc][32 lanes]
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+  // W1 slice: a weight, independent of earlier kernels — TMA boxes in flight before the PDL wait
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"((uint32_t)(ng * kGbRows * 16))
+                 : "memory");
+    for (int g = 0; g < ng; ++g)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%3, %4}], [%2];" ::"r"((uint32_t)__cvta_generic_to_shared(wsm + (size_t)g * kGbRows * 16)),
+          "l"(reinterpret_cast<uint64_t>(&tmap_w)), "r"(bar), "r"(kb + g * G), "r"(o0)
+          : "memory");
+  }
   // X row of request j (row a1): a decode request's single row straight from the caller's
   // embeddings (bit-exact), a prompt's mean from xs (K1).  Only the latter
   // depends on the previous kernel: decode-only steps start without waiting for K1 (PDL).
@@ -88,7 +96,11 @@ trail_gemv_l1_kernel(const T *__restrict__ w1, const T *__restrict__ emb, int64_
   if (__syncthreads_or(pooled)) griddep_wait();
   griddep_launch();
   float *out = partial + (int64_t)s * n * H;
-  const int rg = warp >> 1;                              // 16-row group of this warp
+  const int kh = warp >> 2, tw = warp & 3;               // K half, warp tile
+  const int rq = tw & 1, rr = tw >> 1;                    // 32-request group, 32-row group
+  const int lq = lane & 7, lr = lane >> 3;
+  const int ga = kh ? ng / 2 : 0, gb = kh ? ng : ng / 2;
+  bool w_ready = false;
   for (int j0 = 0; j0 < n; j0 += kGbReq) {
     const int nb = min(kGbReq, n - j0);
     __syncthreads();                                     // previous block's X reads done
@@ -98,71 +110,96 @@ trail_gemv_l1_kernel(const T *__restrict__ w1, const T *__restrict__ emb, int64_
       src[t] = b - a == 1 ? (int64_t)a * ld : -1 - (int64_t)j * d;
     }
     __syncthreads();
-    for (int t = warp; t < nb; t += kWarps) {
+    for (int t = warp; t < nb; t += kWarps) {             // a warp per request row
       const int64_t sj = src[t];
       const T *p = (sj >= 0 ? emb + sj : xs + (-1 - sj)) + kb;
-      for (int q = lane; q < nq; q += 32) cp4<T>(xsm + ((size_t)q * kGbReq + t) * QB, p + 4 * q);
+      for (int g = lane; g < ng; g += 32)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(xsm + ((size_t)g * kGbReq + t) * 16)),
+                     "l"(p + g * G)
+                     : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
-    const int t = (warp & 1) * 32 + lane;                // my request in the block
-    const uint8_t *xp = xsm + (size_t)min(t, nb - 1) * QB;
-    const uint8_t *wp = wsm + (size_t)rg * kGbRpw * QB;
-    float acc[kGbRpw];
-#pragma unroll
-    for (int r = 0; r < kGbRpw; ++r) acc[r] = 0.f;
-    // software pipeline: group q + 1's 17 vectors are loaded while group q's 64 FFMAs issue
-    V xv = *reinterpret_cast<const V *>(xp), wv[kGbRpw];
-#pragma unroll
-    for (int r = 0; r < kGbRpw; ++r) wv[r] = *reinterpret_cast<const V *>(wp + r * QB);
-    for (int q = 0; q < nq; ++q) {
-      const int qn = q + 1 < nq ? q + 1 : q;
-      const V xn = *reinterpret_cast<const V *>(xp + (size_t)qn * kGbReq * QB);
-      V wn[kGbRpw];
-      const uint8_t *wq = wp + (size_t)qn * kGbRows * QB;
-#pragma unroll
-      for (int r = 0; r < kGbRpw; ++r) wn[r] = *reinterpret_cast<const V *>(wq + r * QB);
-      float x[4];
-      Q4<T>::widen(xv, x);
-#pragma unroll
-      for (int r = 0; r < kGbRpw; ++r) {
-        float w[4];
-        Q4<T>::widen(wv[r], w);
-        acc[r] = fmaf(w[0], x[0], acc[r]);
-        acc[r] = fmaf(w[1], x[1], acc[r]);
-        acc[r] = fmaf(w[2], x[2], acc[r]);
-        acc[r] = fmaf(w[3], x[3], acc[r]);
-      }
-      xv = xn;
-#pragma unroll
-      for (int r = 0; r < kGbRpw; ++r) wv[r] = wn[r];
+    if (!w_ready) {
+      uint32_t ok = 0;
+      do {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(ok) : "r"(bar) : "memory");
+      } while (!ok);
+      w_ready = true;
     }
-    if (t < nb) {
-      float4 *dst = reinterpret_cast<float4 *>(out + (int64_t)(j0 + t) * H + o0 + rg * kGbRpw);
+    __syncthreads();
+    float acc[4][8];
 #pragma unroll
-      for (int q = 0; q < kGbRpw / 4; ++q)
-        dst[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) acc[i][r] = 0.f;
+    const uint8_t *xp = xsm + (size_t)(rq * 32 + lq) * 16;
+    const uint8_t *wp = wsm + (size_t)(rr * 32 + lr * 8) * 16;
+#pragma unroll 2
+    for (int g = ga; g < gb; ++g) {
+      float x[4][G], w[8][G];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        G16<T>::widen(*reinterpret_cast<const uint4 *>(xp + ((size_t)g * kGbReq + 8 * i) * 16), x[i]);
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        G16<T>::widen(*reinterpret_cast<const uint4 *>(wp + ((size_t)g * kGbRows + r) * 16), w[r]);
+#pragma unroll
+      for (int e = 0; e < G; ++e)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int r = 0; r < 8; ++r) acc[i][r] = fmaf(w[r][e], x[i][e], acc[i][r]);
+    }
+    if (kh) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) red[((tw * 4 + i) * 8 + r) * 32 + lane] = acc[i][r];
+    }
+    __syncthreads();
+    if (!kh) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int t = rq * 32 + 8 * i + lq;
+        if (t < nb) {
+          float v[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) v[r] = acc[i][r] + red[((tw * 4 + i) * 8 + r) * 32 + lane];
+          float4 *dst = reinterpret_cast<float4 *>(out + (int64_t)(j0 + t) * H + o0 + rr * 32 + lr * 8);
+          dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+          dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+        }
+      }
     }
   }
 }
 
 cudaError_t launch_gemv_l1(const Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
                            int splits, cudaStream_t s) {
-  // split length: a multiple of 8 elements (16-byte copies for bf16 and fp32)
-  const int kchunk = ((c.d + splits - 1) / splits + 7) / 8 * 8;
+  if (!c.have_tmap_gemv) return cudaErrorInvalidValue;
+  const int G = c.dtype == TRAIL_BF16 ? 8 : 4;
+  // split length: a multiple of one 16-byte group
+  const int kchunk = ((c.d + splits - 1) / splits + G - 1) / G * G;
   dim3 grid(c.H / kGbRows, splits);
-  const size_t smem = (size_t)(kGbRows + kGbReq) * kchunk * c.esize + kGbReq * 8;
+  const size_t smem = (size_t)(kGbRows + kGbReq) * kchunk * c.esize + kGbReq * 8 +
+                      (size_t)4 * 32 * 32 * sizeof(float);
   if (smem > (size_t)kGemvSmemMax) return cudaErrorInvalidValue;
   if (c.dtype == TRAIL_BF16)
     return launch_k(trail_gemv_l1_kernel<__nv_bfloat16>, grid, dim3(kWarps * 32), smem, s,
-                    (const __nv_bfloat16 *)c.w1, (const __nv_bfloat16 *)emb, ld, off,
+                    c.tmap_w_gemv, (const __nv_bfloat16 *)emb, ld, off,
                     (const __nv_bfloat16 *)c.xs, n, c.d, c.H, kchunk, c.partial);
-  return launch_k(trail_gemv_l1_kernel<float>, grid, dim3(kWarps * 32), smem, s, (const float *)c.w1,
+  return launch_k(trail_gemv_l1_kernel<float>, grid, dim3(kWarps * 32), smem, s, c.tmap_w_gemv,
                   (const float *)emb, ld, off, (const float *)c.xs, n, c.d, c.H, kchunk, c.partial);
 }
 
-cudaError_t gemv_prepare() {
+cudaError_t gemv_prepare(Ctx &c) {
+  const uint32_t G = c.dtype == TRAIL_BF16 ? 8 : 4;
+  c.have_tmap_gemv = encode_plain_2d(&c.tmap_w_gemv, c.w1, c.dtype == TRAIL_BF16, (uint64_t)c.d,
+                                     (uint64_t)c.H, (uint64_t)c.d, G, kGbRows);
+  if (!c.have_tmap_gemv) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(trail_gemv_l1_kernel<float>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kGemvSmemMax);
   if (e != cudaSuccess) return e;

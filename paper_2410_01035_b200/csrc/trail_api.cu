@@ -85,7 +85,7 @@ void plan_l1(const Ctx &c, int n, int *mode, int *bn, int *splits) {
     // elements and small enough that both operand slices fit in shared memory
     const int ctas_x = c.H / 64;
     int s = std::max(1, c.num_sms / ctas_x);
-    const int kmax = (200 * 1024 - 512) / (128 * (int)c.esize) - 16;
+    const int kmax = (200 * 1024 - 512 - 16384) / (128 * (int)c.esize) - 16;
     s = std::max(s, (c.d + kmax - 1) / kmax);
     s = std::min(s, std::max(1, c.d / 8));
     const int kchunk = ((c.d + s - 1) / s + 7) / 8 * 8;
@@ -334,7 +334,7 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
       cudaMemset(c.xs, 0, (size_t)g.max_requests * c.d * c.esize) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
   if (umma_prepare(c) != cudaSuccess || head_prepare(c) != cudaSuccess ||
-      pool_prepare() != cudaSuccess || gemv_prepare() != cudaSuccess ||
+      pool_prepare() != cudaSuccess || gemv_prepare(c) != cudaSuccess ||
       fused_prepare(c) != cudaSuccess || wide_prepare(c) != cudaSuccess ||
       select_prepare(c) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);

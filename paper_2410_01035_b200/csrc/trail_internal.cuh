@@ -92,6 +92,8 @@ struct Ctx {
   size_t sel_scratch_bytes = 0;
   // TMA descriptors (bf16 path)
   CUtensorMap tmap_x, tmap_w128, tmap_w256;
+  CUtensorMap tmap_w_gemv;                       // W1, 16-byte x 64-row boxes (K2a)
+  bool have_tmap_gemv = false;
   CUtensorMap tmap_xs1, tmap_xs4, tmap_xs32;     // xs rows, boxes 64 x {1, 4, 32} (fused gather)
   CUtensorMap tmap_emb, tmap_emb4, tmap_emb32;   // caller's embeddings, same boxes; re-encoded
                                                  // whenever emb / ld change
@@ -126,7 +128,9 @@ cudaError_t launch_pool(const Ctx &c, const void *emb, int64_t ld, const int32_t
 int pool_grid(const Ctx &c);
 bool pool_use_bulk();
 cudaError_t pool_prepare();
-cudaError_t gemv_prepare();
+cudaError_t gemv_prepare(Ctx &c);
+bool encode_plain_2d(CUtensorMap *m, const void *base, bool bf16, uint64_t cols, uint64_t rows,
+                     uint64_t ld, uint32_t box_cols, uint32_t box_rows);
 cudaError_t launch_gemv_l1(const Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
                            int splits, cudaStream_t s);
 cudaError_t launch_umma_l1(const Ctx &c, int n, int bn, int splits, cudaStream_t s);
