@@ -21,9 +21,10 @@ constexpr int kGemvSmemMax = 200 * 1024;   // W1 + X slices staged in shared mem
 }  // namespace
 
 // Register-tiled GEMV (the kernel K2a launches).  A CTA owns 64 hidden rows x the K range of
-// its split; both operand slices are staged in shared memory "group-major": [K/G][64][G]
-// with G = 16 B of elements (4 fp32 / 8 bf16) — W1 by TMA (one 64-row x 16-byte box per
-// group, issued by one thread before the PDL wait), X by cp.async (rows from emb or xs).
+// its split; W1 is staged in shared memory "group-major": [K/G][64][G] with G = 16 B of
+// elements (4 fp32 / 8 bf16) — by TMA (one 64-row x 16-byte box per
+// group, issued by warp 0 before the PDL wait); X rows by 1-D bulk copies (one per request,
+// from emb or xs) into a row-major layout whose row stride is an odd number of 16-byte units.
 // 8 warps = 2 K halves x 4 warp tiles of 32 requests x 32 rows; lane = 4 requests x 8 rows
 // (requests lq, lq+8, lq+16, lq+24 of its tile: the 8 lanes of a quarter-warp read 8
 // consecutive X vectors, conflict-free; its 8 rows are a shared broadcast per quarter-warp).
@@ -59,10 +60,21 @@ template <typename T>
 __global__ void __launch_bounds__(kWarps * 32, 1)
 trail_gemv_l1_kernel(const __grid_constant__ CUtensorMap tmap_w, const T *__restrict__ emb,
                      int64_t ld, const int32_t *__restrict__ off, const T *__restrict__ xs, int n,
-                     int d, int H, int kchunk, float *__restrict__ partial) {
+                     int d, int H, int kchunk, float *__restrict__ partial,
+                     uint64_t *__restrict__ trace) {
   constexpr int G = G16<T>::G;
+  // diagnostics (trail_trace_*): per-CTA phase timestamps, globaltimer ns
+  uint64_t *tr = trace ? trace + 16 * (int64_t)(blockIdx.x + gridDim.x * blockIdx.y) : nullptr;
+  auto stamp = [&](int i) {
+    if (tr && threadIdx.x == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      tr[i] = t;
+    }
+  };
+  stamp(0);
   extern __shared__ __align__(128) uint8_t gsm[];
-  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ __align__(8) uint64_t s_bar, s_xbar;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int o0 = blockIdx.x * kGbRows;
   const int s = blockIdx.y;
@@ -70,18 +82,26 @@ trail_gemv_l1_kernel(const __grid_constant__ CUtensorMap tmap_w, const T *__rest
   const int kc = max(0, min(d, kb + kchunk) - kb);
   const int ng = kc / G;                                 // 16-byte groups of the K range
   uint8_t *wsm = gsm;                                    // [ng][64 rows][16 B]
-  uint8_t *xsm = gsm + (size_t)ng * kGbRows * 16;        // [ng][64 requests][16 B]
-  int64_t *src = reinterpret_cast<int64_t *>(xsm + (size_t)ng * kGbReq * 16);   // [64]
+  uint8_t *xsm = gsm + (size_t)ng * kGbRows * 16;        // [64 requests][XS]
+  int64_t *src = reinterpret_cast<int64_t *>(xsm + (size_t)kGbReq * (((kchunk * (int)sizeof(T) / 16) | 1) * 16));
   float *red = reinterpret_cast<float *>(src + kGbReq);  // [4 tiles][32 acc][32 lanes]
   const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+  const uint32_t xbar = (uint32_t)__cvta_generic_to_shared(&s_xbar);
+  // X is row-major [64 requests][XS bytes], XS an odd number of 16-byte units (the 8 lanes of
+  // a quarter-warp read 8 consecutive requests at the same K: conflict-free)
+  const int XS = ((kc * (int)sizeof(T) / 16) | 1) * 16;
   // W1 slice: a weight, independent of earlier kernels — TMA boxes in flight before the PDL wait
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(xbar) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                  "r"((uint32_t)(ng * kGbRows * 16))
                  : "memory");
-    for (int g = 0; g < ng; ++g)
+  }
+  __syncwarp();
+  if (warp == 0) {   // the TMA boxes issued by the 32 lanes of warp 0
+    for (int g = lane; g < ng; g += 32)
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
           " [%0], [%1, {%3, %4}], [%2];" ::"r"((uint32_t)__cvta_generic_to_shared(wsm + (size_t)g * kGbRows * 16)),
@@ -93,8 +113,10 @@ trail_gemv_l1_kernel(const __grid_constant__ CUtensorMap tmap_w, const T *__rest
   // depends on the previous kernel: decode-only steps start without waiting for K1 (PDL).
   bool pooled = false;
   for (int j = tid; j < n; j += blockDim.x) pooled |= __ldg(off + j + 1) - __ldg(off + j) != 1;
+  stamp(1);
   if (__syncthreads_or(pooled)) griddep_wait();
   griddep_launch();
+  stamp(2);
   float *out = partial + (int64_t)s * n * H;
   const int kh = warp >> 2, tw = warp & 3;               // K half, warp tile
   const int rq = tw & 1, rr = tw >> 1;                    // 32-request group, 32-row group
@@ -110,17 +132,32 @@ trail_gemv_l1_kernel(const __grid_constant__ CUtensorMap tmap_w, const T *__rest
       src[t] = b - a == 1 ? (int64_t)a * ld : -1 - (int64_t)j * d;
     }
     __syncthreads();
-    for (int t = warp; t < nb; t += kWarps) {             // a warp per request row
-      const int64_t sj = src[t];
-      const T *p = (sj >= 0 ? emb + sj : xs + (-1 - sj)) + kb;
-      for (int g = lane; g < ng; g += 32)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(xsm + ((size_t)g * kGbReq + t) * 16)),
-                     "l"(p + g * G)
+    // X rows: one 1-D bulk copy per request (kc elements), issued by warp 0's lanes
+    if (tid == 0 && kc > 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(xbar),
+                   "r"((uint32_t)(nb * kc * (int)sizeof(T)))
+                   : "memory");
+    else if (tid == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(xbar) : "memory");
+    __syncwarp();
+    if (warp == 0 && kc > 0)
+      for (int t = lane; t < nb; t += 32) {
+        const int64_t sj = src[t];
+        const T *p = (sj >= 0 ? emb + sj : xs + (-1 - sj)) + kb;
+        asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"((uint32_t)__cvta_generic_to_shared(xsm + (size_t)t * XS)), "l"(p),
+                     "r"((uint32_t)(kc * (int)sizeof(T))), "r"(xbar)
                      : "memory");
+      }
+    stamp(3);
+    {
+      const uint32_t xph = (uint32_t)((j0 / kGbReq) & 1);
+      uint32_t ok = 0;
+      do {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(ok) : "r"(xbar), "r"(xph) : "memory");
+      } while (!ok);
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    asm volatile("cp.async.wait_all;" ::: "memory");
     if (!w_ready) {
       uint32_t ok = 0;
       do {
@@ -130,19 +167,20 @@ trail_gemv_l1_kernel(const __grid_constant__ CUtensorMap tmap_w, const T *__rest
       w_ready = true;
     }
     __syncthreads();
+    stamp(4);
     float acc[4][8];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int r = 0; r < 8; ++r) acc[i][r] = 0.f;
-    const uint8_t *xp = xsm + (size_t)(rq * 32 + lq) * 16;
+    const uint8_t *xp = xsm + (size_t)(rq * 32 + lq) * XS;
     const uint8_t *wp = wsm + (size_t)(rr * 32 + lr * 8) * 16;
 #pragma unroll 2
     for (int g = ga; g < gb; ++g) {
       float x[4][G], w[8][G];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        G16<T>::widen(*reinterpret_cast<const uint4 *>(xp + ((size_t)g * kGbReq + 8 * i) * 16), x[i]);
+        G16<T>::widen(*reinterpret_cast<const uint4 *>(xp + (size_t)(8 * i) * XS + (size_t)g * 16), x[i]);
 #pragma unroll
       for (int r = 0; r < 8; ++r)
         G16<T>::widen(*reinterpret_cast<const uint4 *>(wp + ((size_t)g * kGbRows + r) * 16), w[r]);
@@ -175,6 +213,8 @@ trail_gemv_l1_kernel(const __grid_constant__ CUtensorMap tmap_w, const T *__rest
       }
     }
   }
+  __syncthreads();
+  stamp(5);
 }
 
 cudaError_t launch_gemv_l1(const Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
@@ -184,15 +224,18 @@ cudaError_t launch_gemv_l1(const Ctx &c, const void *emb, int64_t ld, const int3
   // split length: a multiple of one 16-byte group
   const int kchunk = ((c.d + splits - 1) / splits + G - 1) / G * G;
   dim3 grid(c.H / kGbRows, splits);
-  const size_t smem = (size_t)(kGbRows + kGbReq) * kchunk * c.esize + kGbReq * 8 +
+  const size_t smem = (size_t)kGbRows * kchunk * c.esize +
+                      (size_t)kGbReq * (((kchunk * c.esize / 16) | 1) * 16) + kGbReq * 8 +
                       (size_t)4 * 32 * 32 * sizeof(float);
   if (smem > (size_t)kGemvSmemMax) return cudaErrorInvalidValue;
+  uint64_t *tr = (c.trace && (int)(grid.x * grid.y) <= c.trace_cap) ? c.trace : nullptr;
   if (c.dtype == TRAIL_BF16)
     return launch_k(trail_gemv_l1_kernel<__nv_bfloat16>, grid, dim3(kWarps * 32), smem, s,
                     c.tmap_w_gemv, (const __nv_bfloat16 *)emb, ld, off,
-                    (const __nv_bfloat16 *)c.xs, n, c.d, c.H, kchunk, c.partial);
+                    (const __nv_bfloat16 *)c.xs, n, c.d, c.H, kchunk, c.partial, tr);
   return launch_k(trail_gemv_l1_kernel<float>, grid, dim3(kWarps * 32), smem, s, c.tmap_w_gemv,
-                  (const float *)emb, ld, off, (const float *)c.xs, n, c.d, c.H, kchunk, c.partial);
+                  (const float *)emb, ld, off, (const float *)c.xs, n, c.d, c.H, kchunk, c.partial,
+                  tr);
 }
 
 cudaError_t gemv_prepare(Ctx &c) {

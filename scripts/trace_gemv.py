@@ -22,7 +22,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 trail_trace_enable(t.h, 4096)
 fl = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-names = ["w1_issue", "pdl_wait", "x_issue", "landed", "compute"]
+names = ["w1_issue+scan", "pdl_wait", "x_issue", "landed", "compute"]
 for it in range(4):
     fl.zero_()
     torch.cuda.synchronize()
