@@ -72,17 +72,45 @@ def peaks():
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML every ~2 ms from a
+    thread (the timed region is tens of ms, too short for nvidia-smi's 100 ms loop), with
+    nvidia-smi as the fallback when NVML is unavailable."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
         self.lines = []
+        self.nv = None
+        self.samples = []          # (sm_mhz, max_mhz, reasons)
+        self._stop = threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            bits = {"hw_slowdown": pynvml.nvmlClocksThrottleReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksThrottleReasonSwPowerCap}
+            mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.nv = (pynvml, h, bits, mx)
+
+            def loop():
+                while not self._stop.is_set():
+                    sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                    self.samples.append((sm, mx, {nm for nm, b in bits.items() if r & b}))
+                    time.sleep(0.002)
+            self._t = threading.Thread(target=loop, daemon=True)
+            self._t.start()
+            return self
+        except Exception:
+            self.nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
@@ -100,10 +128,14 @@ class ClockSampler:
 
     def wait_first_sample(self, timeout: float = 5.0):
         t0 = time.time()
-        while self.proc and not self.lines and time.time() - t0 < timeout:
-            time.sleep(0.02)
+        while (self.nv or self.proc) and not (self.lines or self.samples) and \
+                time.time() - t0 < timeout:
+            time.sleep(0.002)
 
     def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self._t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -113,7 +145,10 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s_, m_, r_ in list(self.samples):
+            sm.append(s_)
+            mx = max(mx, m_)
+            reasons |= r_
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
@@ -123,11 +158,12 @@ class ClockSampler:
                 mx = max(mx, float(parts[2]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[5:9]):
+            for nm, v in zip(self.NAMES, parts[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------------------- workload
