@@ -10,4 +10,4 @@ timeout 600 python bench.py --config c4 --steps 20 --warmup 5 --cpu-seconds 5 > 
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 5 --warmup 3 --no-cpu > gpurun_out/ncu_bench.log 2>&1; echo "ncu1 exit $?" >> gpurun_out/ncu_bench.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fused|rank|pool" -c 8 -o gpurun_out/prof_full python bench.py --steps 2 --warmup 3 --no-cpu --no-graph > gpurun_out/ncu_full.log 2>&1; echo "ncu2 exit $?" >> gpurun_out/ncu_full.log
 python scripts/ncu_summary.py gpurun_out/prof_full.ncu-rep > gpurun_out/ncu_full_summary.csv 2>&1
-tail -2 gpurun_out/gpu_tests.log; tail -1 gpurun_out/smoke.log; tail -1 gpurun_out/bench_full.err; cat gpurun_out/bench_ref.json; tail -1 gpurun_out/ncu_bench.log gpurun_out/ncu_full.log
+tail -n 2 gpurun_out/gpu_tests.log; for f in gpurun_out/smoke.log gpurun_out/bench_full.err gpurun_out/ncu_bench.log gpurun_out/ncu_full.log; do tail -n 1 "$f"; done; cat gpurun_out/bench_ref.json
