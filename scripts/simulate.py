@@ -63,6 +63,7 @@ def run(c: float, args, seed: int) -> dict:
     done = np.full(n_jobs, -1, np.int64)
     running = set()
     observed = set()
+    recompute = np.zeros(n_jobs, np.int64)   # iterations of context recompute still owed
     nxt, it, preempt = 0, 0, 0
     dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
     while (nxt < n_jobs or live) and it < args.max_iters:
@@ -86,7 +87,27 @@ def run(c: float, args, seed: int) -> dict:
         if not batch:                    # forced set over budget with nothing runnable
             it += 1
             continue
-        # one token each, then observe the jobs that ran
+        # discard mode: a preempted job lost its KV; when it runs again it first
+        # rebuilds its context at recompute_rate tokens per iteration, emitting nothing
+        if args.recompute_rate > 0:
+            for j in running - set(batch):
+                if gen[j] < size[j]:
+                    recompute[j] = -1                 # owed once re-admitted
+            for j in batch:
+                if recompute[j] == -1:
+                    recompute[j] = int(math.ceil((plen[j] + gen[j]) / args.recompute_rate))
+        emit = []
+        for j in batch:
+            if recompute[j] > 0:
+                recompute[j] -= 1
+                continue
+            emit.append(j)
+        running = set(batch)
+        batch = emit
+        if not batch:
+            it += 1
+            continue
+        # one token each, then observe the jobs that emitted
         for j in batch:
             if first[j] < 0:
                 first[j] = it
@@ -101,7 +122,6 @@ def run(c: float, args, seed: int) -> dict:
         t.predict(dv(W.encode(emb, "bf16").view(np.int16)), dv(np.arange(len(batch) + 1, dtype=np.int32)),
                   dv(np.array([live[j] for j in batch], np.int32)), dv(pref))
         observed.update(batch)
-        running = set(batch)
         fin = [j for j in batch if gen[j] >= size[j]]
         if fin:
             t.release(dv(np.array([live[j] for j in fin], np.int32)))
@@ -130,6 +150,8 @@ def main():
     ap.add_argument("--conc", type=float, default=2.0)
     ap.add_argument("--mislabel", type=float, default=0.1)
     ap.add_argument("--c", default="0,0.5,0.8,inf")
+    ap.add_argument("--recompute-rate", type=float, default=0.0,
+                    help="discard mode: tokens of context rebuilt per iteration (0 = hold mode)")
     ap.add_argument("--seeds", type=int, default=2)
     ap.add_argument("--max-iters", type=int, default=200000)
     args = ap.parse_args()
