@@ -625,9 +625,13 @@ def run_reference(args, cfg):
         "n_gpus": world, "steps": n_steps, "warmup": args.warmup, "ms_per_step": ms,
         "us_per_iteration": ms * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-        "config": {"workload": cfg["desc"], "n_per_gpu": cfg["n"], "d": cfg["d"], "bins": cfg["k"],
-                   "c": cfg["c"], "note": "the fp64 CPU oracle (oracle/trail_ref.py) is the "
-                                          "reference arm: the paper ships no code"},
+        "config": {"workload": f"BASELINE configs[{ {'c1': 0, 'c2': 1, 'c4': 3}[args.config] }]" +
+                               (f" / configs[2] shape at N={world}" if world > 1 else "") +
+                               ": " + cfg["desc"],
+                   "n_per_gpu": cfg["n"], "waiting_per_gpu": cfg["waiting"], "d": cfg["d"],
+                   "hidden": cfg["H"], "bins": cfg["k"], "c": cfg["c"],
+                   "note": "the fp64 CPU oracle (oracle/trail_ref.py) is the reference arm: the "
+                           "paper ships no code"},
         "cpu_baseline": {"value": val, "unit": "requests/s", "cores": _threads(), "kind": "oracle",
                          "sample": f"{n_steps} full steps, rank 0 only"},
         "e2e": {"value": val, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
