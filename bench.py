@@ -370,9 +370,10 @@ def run_ours(args, cfg):
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp) and args.config == "c2" and world == 1:
+    if os.path.exists(tp) and world == 1:
         with open(tp) as f:
-            traffic = json.load(f).get(dom)
+            tj = json.load(f)
+        traffic = tj.get(dom) if args.config == "c2" else tj.get(f"{dom}_{args.config}")
     if roof is not None:
         roof.update({"kernel": dom, "peak_source": peak_src, "avg_launch_us": avg[dom] * 1e3,
                      "traffic": traffic,
