@@ -97,9 +97,13 @@ def softmax(z: np.ndarray) -> np.ndarray:
 
 def init_posterior(p: np.ndarray, prior: np.ndarray) -> np.ndarray:
     """q^(0) = normalise(pi * p^(0)); with a uniform pi this is P:219 'Initialize
-    q^(0) = p^(0)'.  A per-request pi (e.g. a BERT prompt prior) is reading D-9."""
+    q^(0) = p^(0)'.  A per-request pi (e.g. a BERT prompt prior) is reading D-9.  A prior
+    with no mass where p has any (normaliser < 1e-300) falls back to p, as the update does
+    (reading D-5)."""
     num = prior * p
-    return num / num.sum(axis=-1, keepdims=True)
+    Z = num.sum(axis=-1, keepdims=True)
+    safe = Z >= 1e-300
+    return np.where(safe, num / np.where(safe, Z, 1.0), p)
 
 
 def bayes_update(q_prev: np.ndarray, p: np.ndarray, T: np.ndarray) -> np.ndarray:
@@ -299,7 +303,11 @@ class TrailOracle:
                       np.asarray(ids, dtype=np.int64) + id_base, kv_budget, max_run)
 
     def release(self, ids) -> None:
+        """A finished (or aborted) request frees its slot: the slot is unseen again and any
+        partial chunked-prefill rows it had accumulated (D-27) are dropped."""
         self.state.release(ids)
+        for sid in np.asarray(ids, dtype=np.int64).ravel():
+            getattr(self, "_chunks", {}).pop(int(sid), None)
 
 
 def select(key, forced, arrival_seq, kv_blocks, is_running, ids, kv_budget: int,

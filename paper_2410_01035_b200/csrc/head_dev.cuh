@@ -32,7 +32,7 @@ __device__ __forceinline__ float seg_sum(float v, int seg) {
 //   decode:  log q = logaddexp(log T_bb + lq(b), log T_b,b+1 + lq(b+1)) + log p
 //   normalise; L = sum_b q(b) m_b
 // Five segment reductions: max z, sum exp, (max, argmax) of the unnormalised log q, sum exp,
-// sum q m.  The D-5 fallback (all-zero product) needs max log p = max z - lse: no reduction.
+// sum q m.  The D-5 fallback (all-zero product) redoes the (max, argmax) over log p.
 __device__ __forceinline__ void head_seg(int j, int n, int k, int SEG, int b, float z,
                                          const HeadSmem &hc, float hc_dyn_c, uint32_t sl,
                                          const SlotMeta &mt,
@@ -72,10 +72,15 @@ __device__ __forceinline__ void head_seg(int j, int n, int k, int SEG, int b, fl
     const int oi = __shfl_xor_sync(0xffffffffu, bi, o, SEG);
     if (ov > qmax || (ov == qmax && oi < bi)) { qmax = ov; bi = oi; }
   }
-  if (qmax == -INFINITY) {          // all-zero product: fall back to p (D-5)
-    lq = lp;
-    qmax = zmax - lse;
-    bi = 0;                         // (only reachable for a zero prior on every bin)
+  if (qmax == -INFINITY) {          // all-zero product: fall back to p (D-5); only reachable
+    lq = lp;                        // for a prior that is zero on every bin.  The argmax is
+    qmax = lq;                      // redone over p, as K3 and the oracle do.
+    bi = act ? b : 0x7FFFFFFF;
+    for (int o = SEG >> 1; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, qmax, o, SEG);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o, SEG);
+      if (ov > qmax || (ov == qmax && oi < bi)) { qmax = ov; bi = oi; }
+    }
   }
   const float qs = seg_sum(act ? __expf(lq - qmax) : 0.f, SEG);   // every lane shuffles
   lq = act ? lq - (qmax + __logf(qs)) : -INFINITY;

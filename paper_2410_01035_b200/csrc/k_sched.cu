@@ -323,10 +323,28 @@ __global__ void trail_release_kernel(const uint32_t *__restrict__ ids, int n, in
   meta[slot] = m;
 }
 
+// a released slot also drops any partial chunked-prefill sum (K1c, reading D-27): a request
+// aborted between two chunks must not leak its rows into the slot's next prompt.  A CTA per
+// id, one thread per float4 of the row.
+__global__ void trail_release_chunks_kernel(const uint32_t *__restrict__ ids, int n, int d,
+                                            int max_slots, float *__restrict__ acc,
+                                            uint32_t *__restrict__ cnt) {
+  griddep_wait();
+  griddep_launch();
+  const uint32_t slot = ids[blockIdx.x];
+  if (slot >= (uint32_t)max_slots) return;
+  float4 *row = reinterpret_cast<float4 *>(acc + (int64_t)slot * d);
+  for (int v = threadIdx.x; v < d / 4; v += blockDim.x) row[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x == 0) cnt[slot] = 0u;
+}
+
 cudaError_t launch_release(const Ctx &c, const uint32_t *ids, int n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   trail_release_kernel<<<(n + 255) / 256, 256, 0, s>>>(ids, n, c.cfg.max_slots, c.meta,
                                                        c.dev_err);
+  if (c.chunk_acc)
+    trail_release_chunks_kernel<<<n, 256, 0, s>>>(ids, n, c.d, c.cfg.max_slots, c.chunk_acc,
+                                                  c.chunk_cnt);
   return cudaGetLastError();
 }
 

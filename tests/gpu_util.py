@@ -81,3 +81,17 @@ def assert_predict_close(qg, Lg, qo, Lo, what=""):
 def top2_gap(q):
     s = np.sort(q, axis=-1)
     return s[..., -1] - s[..., -2]
+
+
+def report_exemptions(name: str, record: dict) -> None:
+    """Write a parity run's near-tie exemptions (the comparator reports every
+    exemption) to gpurun_out/parity_exemptions/<name>.json, visible after `-q` runs."""
+    import json
+    import os
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "gpurun_out", "parity_exemptions")
+    os.makedirs(root, exist_ok=True)
+    with open(os.path.join(root, name + ".json"), "w") as f:
+        json.dump(record, f, indent=1)
+    print(f"{name}: {record.get('key_exempt_steps')} steps with key near-tie exemptions, "
+          f"{len(record.get('exemptions', []))} exempted ids")

@@ -14,7 +14,7 @@ from oracle import trail_ref as R  # noqa: E402
 from synth import workload as W  # noqa: E402
 
 from gpu_util import (assert_predict_close, dev, gpu_keys_forced, gpu_predict, gpu_schedule,  # noqa: E402
-                      gpu_state, make_pair, oracle_predict, top2_gap)
+                      gpu_state, make_pair, oracle_predict, report_exemptions, top2_gap)
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -162,6 +162,32 @@ def test_prior_override_and_uniform_reduces_to_softmax():
     qg2, _ = gpu_predict(t, emb, off, ids, pref)
     p = o.probs(o.pooled_inputs(W.decode(emb, "bf16"), off))
     assert np.abs(qg2 - p).max() <= 2e-3
+
+
+@pytest.mark.parametrize("l1", [1, 2, 4])
+def test_prior_override_zero_support_falls_back_to_p(l1):
+    """Per-request priors with zeros, including rows with no mass anywhere: q^(0) falls back
+    to p (reading D-5) and the threshold comes from argmax p on every head (K3 on the GEMV
+    path, the K2c / K2d epilogue head) exactly as in the oracle."""
+    n, d, k = 48, 1024, 10
+    w = W.make_weights(d, 512, k, "bf16", seed=5)
+    t, o = make_pair(w, 0.8, n, n, n, "bf16", l1_mode=l1)
+    ids = np.arange(n, dtype=np.uint32)
+    rs = np.random.default_rng(6)
+    pri = rs.dirichlet(np.ones(k), size=n)
+    pri[rs.random((n, k)) < 0.5] = 0.0
+    pri[::3] = 0.0                                   # no support at all
+    pri[1::3, 0] = 1.0
+    pri = (pri / np.maximum(pri.sum(axis=1, keepdims=True), 1e-30)).astype(np.float32)
+    emb, off, pref = W.make_step_inputs(n, d, "bf16", prefill_frac=1.0, seed=7)
+    qg, Lg = gpu_predict(t, emb, off, ids, pref, prior_override=pri)
+    qo, Lo = oracle_predict(o, emb, off, ids, pref, "bf16", prior_override=pri.astype(np.float64))
+    assert_predict_close(qg, Lg, qo, Lo)
+    gap = np.array([top2_gap(q) for q in qo])
+    thr = gpu_state(t, ids)["thr"]
+    ok = gap >= 2e-3
+    np.testing.assert_array_equal(thr[ok], o.state.thr[ids[ok].astype(np.int64)])
+    t.close()
 
 
 def test_decode_on_unseen_slot_is_first_observation_and_release():
@@ -328,6 +354,7 @@ def test_closed_loop_trajectory(cfg):
     w = W.make_weights(d, 512, 10, dtype, seed=21)
     t, o = make_pair(w, c, eng.max_slots, eng.max_slots, eng.max_slots, dtype)
     key_exempt = 0
+    exemptions = []
     max_rl = 0.0
     q0gap = {}
     for step in range(cfg["steps"]):
@@ -358,7 +385,9 @@ def test_closed_loop_trajectory(cfg):
                                b.sched_ids.astype(np.int64), b.kv_budget)
         # forced flags may differ only through an argmax near-tie of q^(0) (contract iii)
         for j in np.nonzero(gf != of_)[0]:
-            assert q0gap.get(int(b.sched_ids[j]), 0.0) < 2e-3, f"step {step}: forced flag"
+            gap = q0gap.get(int(b.sched_ids[j]), 0.0)
+            assert gap < 2e-3, f"step {step}: forced flag"
+            exemptions.append(dict(step=step, kind="forced", id=int(b.sched_ids[j]), q0_top2_gap=gap))
         if set(r3) != set(run):
             diff = set(r3) ^ set(run)
             pos = {int(s): i for i, s in enumerate(b.sched_ids)}
@@ -372,10 +401,19 @@ def test_closed_loop_trajectory(cfg):
                 near_key = abs(ok_[j] - cut) <= eps * max(cut, 1.0)
                 assert near_key or near_forced, f"step {step}: id {s} not a near-tie"
                 key_only |= not near_forced
+                exemptions.append(dict(step=step, kind="forced" if near_forced else "key",
+                                       id=int(s), rel_gap_to_cut=float(abs(ok_[j] - cut) / max(cut, 1.0)),
+                                       band=eps))
             key_exempt += int(key_only)
         eng.advance(run)
-    print(f"closed loop {cfg}: {key_exempt} steps with near-tie exemptions, "
-          f"max rel dL {max_rl:.2e}, tie band {min(1e-3, max(1e-6, 4 * max_rl)):.2e}")
+    # every exemption is reported and their number is bounded (DESIGN.md §5:
+    # at most one step in ten, at least 2, may show a key near-tie at the budget cutoff)
+    report_exemptions(f"closed_loop_{cfg['n']}_{cfg['dtype']}_c{cfg['c']}_{cfg['temporal']}",
+                      dict(cfg={k: (str(v) if isinstance(v, float) and math.isinf(v) else v)
+                                for k, v in cfg.items()},
+                           key_exempt_steps=key_exempt, max_rel_dL=max_rl,
+                           tie_band=min(1e-3, max(1e-6, 4 * max_rl)), exemptions=exemptions))
+    assert key_exempt <= max(2, cfg["steps"] // 10), (key_exempt, exemptions)
 
 
 def test_cuda_graph_capture_matches_eager():
@@ -597,3 +635,43 @@ def test_chunked_prefill(dtype, d, l1):
     qo, Lo = oracle_predict(o, ref_store, off1, ids, pref, dtype)
     assert_predict_close(qg, Lg, qo, Lo, "chunked prefill")
     t.close()
+
+
+@pytest.mark.parametrize("dtype,d", [("bf16", 1024), ("f32", 512)])
+def test_release_mid_prefill_drops_partial_chunks(dtype, d):
+    """A request aborted between two prefill chunks and released: the slot's next prompt
+    is pooled over its own rows only (trail_release clears the K1c running sum + count;
+    the oracle's release drops its chunk list).  Compared bit-for-bit with the same slot
+    pooled on a fresh handle, and with the oracle."""
+    from paper_2410_01035_b200.trail import trail_prefill_chunk
+    w = W.make_weights(d, 512, 10, dtype, seed=91)
+    rs = np.random.default_rng(92)
+    a = W.make_step_inputs(1, d, dtype, prefill_frac=1.0, mean_prompt=37, seed=93)[0]
+    b = W.make_step_inputs(1, d, dtype, prefill_frac=1.0, mean_prompt=11, seed=94)[0]
+    outs = []
+    for aborted in (True, False):
+        t, o = make_pair(w, 0.8, 4, 4, 4, dtype)
+        ids = np.array([2], np.uint32)
+        pooled = torch.empty((1, d), dtype=torch.uint16 if dtype == "bf16" else torch.float32,
+                             device="cuda")
+        if aborted:   # first chunk of prompt a, then the request is aborted and released
+            off = np.array([0, a.shape[0]], np.int32)
+            trail_prefill_chunk(t.h, dev(a), d, dev(off), dev(ids), dev(np.zeros(1, np.uint8)), 1,
+                                pooled, d)
+            o.prefill_chunk(W.decode(a, dtype), off, ids, np.zeros(1, np.uint8))
+            t.release(dev(ids))
+            o.release(ids)
+        off = np.array([0, b.shape[0]], np.int32)
+        trail_prefill_chunk(t.h, dev(b), d, dev(off), dev(ids), dev(np.ones(1, np.uint8)), 1,
+                            pooled, d)
+        torch.cuda.synchronize()
+        ref = o.prefill_chunk(W.decode(b, dtype), off, ids, np.ones(1, np.uint8))
+        got = pooled.cpu().numpy()
+        outs.append(got.copy())
+        g = W.decode(got.view(np.uint16) if dtype == "bf16" else got, dtype)
+        tol = np.abs(ref) * (2.0 ** -7 if dtype == "bf16" else 1e-5) + 1e-6
+        assert np.all(np.abs(g - ref) <= tol)
+        np.testing.assert_allclose(ref[0], W.decode(b, dtype).mean(axis=0) if dtype == "f32"
+                                   else ref[0])
+        t.close()
+    np.testing.assert_array_equal(outs[0], outs[1])

@@ -119,11 +119,84 @@ def test_uniform_prior_reduces_to_softmax():
     np.testing.assert_allclose(q, p, rtol=1e-13)
 
 
-def test_L_minus_one_identity_pins_orientation_and_posterior_feeding():
+def test_init_posterior_weights_by_prior():
+    """q^(0) = normalise(pi * p^(0)) with a non-uniform pi (D-9; P:219 is the uniform case).
+    Hand-computed goldens (tests/golden/prior_weighting.json): an oracle that ignored pi
+    or divided by it fails every case."""
+    g = _golden("prior_weighting.json")
+    for case in g["init_posterior"]:
+        pi, p = np.array([case["prior"]]), np.array([case["p"]])
+        np.testing.assert_allclose(R.init_posterior(p, pi)[0], case["q0"], rtol=0, atol=1e-15)
+
+
+def test_prior_moves_the_initial_prediction_and_threshold():
+    """r = m[argmax q^(0)] with q^(0) prior-weighted: pi = [0.75, 0.25] turns
+    p = [0.4, 0.6] into q^(0) = [2/3, 1/3], so r = m_0 and floor(0.8 r) = 0; a uniform
+    prior keeps r = m_1 (golden).  Checked through TrailOracle's prefill bookkeeping."""
+    case = _golden("prior_weighting.json")["init_posterior"][2]
+    e, p = np.array(case["edges"]), np.array([case["p"]])
+    m = R.bin_midpoints(e)
+    q0 = R.init_posterior(p, np.array([case["prior"]]))
+    assert R.initial_prediction(q0, m)[0] == case["r"]
+    assert R.preempt_threshold(0.8, R.initial_prediction(q0, m))[0] == case["thr_c08"]
+    qu = R.init_posterior(p, np.full((1, 2), 0.5))
+    assert R.initial_prediction(qu, m)[0] == case["r_uniform"]
+    assert R.preempt_threshold(0.8, R.initial_prediction(qu, m))[0] == case["thr_c08_uniform"]
+    # the same through the stateful oracle: a 1-d probe whose logits are log p exactly
+    o = R.TrailOracle(np.zeros((1, 1)), np.zeros(1), np.zeros((2, 1)), np.log(p[0]), e, 0.8, 2,
+                      prior=np.array(case["prior"]), x_dtype="f32")
+    q, L = o.predict_step(np.zeros((1, 1)), np.array([0, 1]), np.array([0]), np.array([1]))
+    np.testing.assert_allclose(q[0], case["q0"], atol=1e-15)
+    assert o.state.thr[0] == case["thr_c08"]
+
+
+def test_prior_mean_length_non_uniform():
+    """E_pi[L] = sum_i pi_i m_i (D-24) for non-uniform pi, hand-computed (golden): 76.8 on
+    the paper bins for pi = [0.4, 0.3, 0.2, 0.1, 0, ...]; 1.5 on edges [0, 2, 4].  Also the
+    key of an unseen request in an oracle created with that prior."""
+    g = _golden("prior_weighting.json")["prior_mean_length"]
+    e0 = W.paper_bin_edges(10)
+    assert R.prior_mean_length(e0, np.array(g[0]["prior"])) == pytest.approx(g[0]["E_L"], abs=1e-12)
+    assert R.prior_mean_length(np.array(g[1]["edges"]), np.array(g[1]["prior"])) == \
+        pytest.approx(g[1]["E_L"], abs=1e-15)
+    w = W.make_weights(16, 8, 10, "f32")
+    o = R.TrailOracle(w["W1"], w["b1"], w["W2"], w["b2"], e0, 0.8, 4,
+                      prior=np.array(g[0]["prior"]), x_dtype="f32")
+    key, forced = o.keys_and_forced(np.array([2]), np.array([0]))
+    assert key[0] == pytest.approx(g[0]["E_L"], abs=1e-12) and not forced[0]
+
+
+def test_two_step_refinement_is_posterior_fed():
+    """Reading D-2 pinned by a hand-computed two-step example (golden two_step): the prior
+    of step t is T applied to the previous POSTERIOR, giving q^(2) = [9/13, 4/13]
+    and L = 21/13; the literal prior-fed recursion of P:220 would give [3/7, 4/7]."""
+    g = _golden("prior_weighting.json")["two_step"]
+    e = np.array(g["edges"])
+    T, m = R.transition_matrix(e), R.bin_midpoints(e)
+    p = np.array(g["p"])
+    q = R.init_posterior(p[:1], np.full((1, 2), 0.5))
+    q = R.bayes_update(q, p[1:2], T)
+    np.testing.assert_allclose(q[0], g["q1"], atol=1e-15)
+    q = R.bayes_update(q, p[2:3], T)
+    np.testing.assert_allclose(q[0], g["q2"], atol=1e-15)
+    assert R.expected_length(q, m)[0] == pytest.approx(g["L2"], abs=1e-15)
+    assert abs(q[0, 0] - g["q2_prior_fed"][0]) > 0.2
+    # and through the stateful oracle (three observations of one slot)
+    o = R.TrailOracle(np.zeros((1, 1)), np.zeros(1), np.zeros((2, 1)), np.zeros(2), e, 0.8, 1,
+                      x_dtype="f32")
+    for t in range(3):
+        o.b2 = np.log(p[t])
+        q, L = o.predict_step(np.zeros((1, 1)), np.array([0, 1]), np.array([0]),
+                              np.array([1 if t == 0 else 0]))
+    np.testing.assert_allclose(q[0], g["q2"], atol=1e-15)
+
+
+def test_L_minus_one_identity_pins_orientation():
     """Closed form (derived in DESIGN.md §4): equal widths w, m_0 = w/2, uninformative p:
     L' = (L - 1 + q_0/2) / (1 - q_0/w); so L' = L - 1 exactly when q_0 = 0.  The other T
-    orientation would give L + 1; a prior-fed recursion would not track q_0 of the
-    posterior.  Checked over 40 chained steps fed by the previous posterior."""
+    orientation would give L + 1 (reading D-1).  With a uniform p the prior-fed and
+    posterior-fed recursions coincide up to normalisation, so this pins D-1 only; D-2 is
+    pinned by test_two_step_refinement_is_posterior_fed."""
     e = W.paper_bin_edges(10)
     m, T, w = R.bin_midpoints(e), R.transition_matrix(e), 51.2
     rs = np.random.default_rng(7)
@@ -344,3 +417,9 @@ def test_prefill_chunk_oracle_is_the_mean_of_all_rows():
     ob.prefill_chunk(xb[:10], np.array([0, 10]), np.array([1]), np.array([0]))
     out = ob.prefill_chunk(xb[10:], np.array([0, 27]), np.array([1]), np.array([1]))
     np.testing.assert_array_equal(out[0], R.bf16_round(xb.mean(axis=0)))
+    # a request aborted between chunks and released: the slot's next prompt pools only its
+    # own rows (numpy mean of that prompt), not the aborted one's partial rows
+    o.prefill_chunk(full[:20], np.array([0, 20]), np.array([5]), np.array([0]))
+    o.release(np.array([5]))
+    nxt = o.prefill_chunk(full[20:], np.array([0, 17]), np.array([5]), np.array([1]))
+    np.testing.assert_allclose(nxt[0], full[20:].mean(axis=0), rtol=1e-12, atol=1e-15)
