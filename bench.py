@@ -15,7 +15,8 @@ rank holds 512 requests (configs[2] at N = 8: 4096 requests over 8 B200): weak s
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c4] [--impl ours|reference]
 
 Inputs are synthetic (synth/, seeded) and resident in HBM before the timed region; L2 is
-flushed (256 MiB memset) between timed steps, outside the per-step CUDA-event brackets.
+flushed (256 MiB memset + 256 MiB read of another buffer) between timed steps, outside the
+per-step CUDA-event brackets.
 Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
@@ -46,7 +47,7 @@ CONFIGS = {
     "c1": dict(n=64, waiting=16, d=4096, H=512, k=10, dtype="f32", c=0.8, total=512.0,
                desc="64 running requests, d=4096, MLP 4096->512->10, fp32"),
     "c4": dict(n=16384, waiting=4096, d=8192, H=512, k=20, dtype="bf16", c=0.8, total=1024.0,
-               burst=False, distinct=4,
+               burst=False, distinct=4, strong=True,
                desc="16384 requests/GPU at d=8192 (70B-shaped), 20 bins, tcgen05 GEMM regime"),
 }
 
@@ -197,17 +198,57 @@ def algorithmic_bytes_l1(cfg, n):
     return cfg["H"] * cfg["d"] * eb + n * cfg["d"] * eb
 
 
-def run_ours(args, cfg):
+def log(*a):
+    """Progress on stderr (the JSON line alone goes to stdout)."""
+    print(f"[bench {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
+
+
+def per_rank(cfg, world):
+    """Requests on one rank: configs[3] (c4) is strong scaling (16 384 requests in total over
+    N GPUs, BASELINE.json configs[3] 'at 1/2/4/8 GPUs'); c2/c1 are weak (n per GPU, c2 at
+    N = 8 is configs[2])."""
+    if cfg.get("strong"):
+        return dict(cfg, n=cfg["n"] // world, waiting=cfg["waiting"] // world)
+    return cfg
+
+
+def run_ours(args):
     import torch
     import torch.distributed as dist
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
+    out = measure(args, args.config, rank, world, local, device, main=True)
+    subs = [c for c in args.sub.split(",") if c and c != args.config]
+    if subs and out is not None:
+        out["sub_configs"] = {}
+    for c in subs:
+        o = measure(args, c, rank, world, local, device, main=False)
+        if out is not None:
+            out["sub_configs"][c] = {k: o[k] for k in (
+                "value", "unit", "ms_per_step", "us_per_iteration", "step_us", "scaling",
+                "dtype", "config", "roofline", "burst_prefill", "cpu_baseline", "e2e",
+                "gpu_launches") if k in o}
+            out["gpu_launches_sub"] = out.get("gpu_launches_sub", 0) + o["gpu_launches"]
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def measure(args, cfg_name, rank, world, local, device, main):
+    import torch
+    import torch.distributed as dist
+
+    cfg = per_rank(CONFIGS[cfg_name], world)
+    log(f"{cfg_name}: building {cfg['n']} requests x {cfg['d']} inputs")
     from paper_2410_01035_b200 import (Trail, load_library, trail_comm_init,
                                        trail_nccl_unique_id, trail_plan_l1,
                                        trail_profile_enable, trail_profile_read)
@@ -238,7 +279,7 @@ def run_ours(args, cfg):
     dev = [mk(b) for b in batches]
     dev_init = mk(init)
     stream = torch.cuda.Stream(device)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+    flush = L2Flush(torch, device)
 
     def step_x(x):
         t.predict(x["emb"], x["off"], x["ids"], x["pref"], stream=stream)
@@ -247,6 +288,7 @@ def run_ours(args, cfg):
     def step(i):
         step_x(dev[i % nb])
 
+    log(f"{cfg_name}: inputs resident; eager warm-up")
     # burst prefill (initialises every slot), then one eager pass over the cycled batches
     with torch.cuda.stream(stream):
         step_x(dev_init)
@@ -283,6 +325,7 @@ def run_ours(args, cfg):
             with torch.cuda.stream(stream):
                 step(i)
 
+    log(f"{cfg_name}: graphs captured; timing {args.steps} steps")
     kernels = ["pool", "gemv", "umma", "head", "pack", "select", "gather"]
     for i in range(args.warmup):
         run_step(i)
@@ -298,7 +341,7 @@ def run_ours(args, cfg):
         for i in range(args.steps):
             if not args.no_flush:
                 with torch.cuda.stream(stream):
-                    flush.zero_()
+                    flush()
             ev[i][0].record(stream)
             run_step(args.warmup + i)
             ev[i][1].record(stream)
@@ -312,7 +355,7 @@ def run_ours(args, cfg):
     for i in range(min(args.steps, 50)):
         if not args.no_flush:
             with torch.cuda.stream(stream):
-                flush.zero_()
+                flush()
         run_step(args.warmup + i, prof=True)
         stream.synchronize()
         for kname in kernels:
@@ -373,7 +416,7 @@ def run_ours(args, cfg):
     if os.path.exists(tp) and world == 1:
         with open(tp) as f:
             tj = json.load(f)
-        traffic = tj.get(dom) if args.config == "c2" else tj.get(f"{dom}_{args.config}")
+        traffic = tj.get(dom) if cfg_name == "c2" else tj.get(f"{dom}_{cfg_name}")
     if roof is not None:
         roof.update({"kernel": dom, "peak_source": peak_src, "avg_launch_us": avg[dom] * 1e3,
                      "traffic": traffic,
@@ -391,7 +434,7 @@ def run_ours(args, cfg):
         for _ in range(5):
             a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             with torch.cuda.stream(stream):
-                flush.zero_()
+                flush()
                 a.record(stream)
                 step_x(dev_init)
                 b2.record(stream)
@@ -409,6 +452,7 @@ def run_ours(args, cfg):
                  "pool_frac_of_hbm": byts / (pool_ms / 1e3) / 1e9 / hbm}
 
     # ---- end to end through the C ABI with HOST buffers (pinned), copies in the timed region
+    log(f"{cfg_name}: device-timed {ms_per_step * 1e3:.1f} us/step; e2e")
     e2e = run_e2e(args, cfg, t, batches, stream, flush, torch, device, world)
 
     # ---- gpu launches of our kernels in the timed region
@@ -419,7 +463,11 @@ def run_ours(args, cfg):
 
     out = None
     if rank == 0:
-        cpu = cpu_baseline(cfg, args) if (world == 1 and not args.no_cpu) else None
+        log(f"{cfg_name}: e2e {e2e['ms_per_step'] * 1e3:.1f} us/step; CPU oracle baseline")
+        cpu = (cpu_baseline(cfg, args, args.cpu_seconds if main else args.cpu_seconds / 3,
+                            prebuilt=(eng, init, batches))
+               if (world == 1 and not args.no_cpu) else None)
+        st = sorted(step_ms)
         out = {
             "metric": "predict+schedule requests/s",
             "value": value,
@@ -429,19 +477,24 @@ def run_ours(args, cfg):
             "warmup": args.warmup,
             "ms_per_step": ms_per_step,
             "us_per_iteration": ms_per_step * 1e3,
+            "step_us": {"mean": ms_per_step * 1e3, "median": 1e3 * statistics.median(st),
+                        "p99": 1e3 * st[min(len(st) - 1, int(math.ceil(0.99 * len(st))) - 1)],
+                        "min": 1e3 * st[0], "max": 1e3 * st[-1],
+                        "note": "rank-local CUDA-event step times (value uses the max over "
+                                "ranks of the total)"},
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if cfg.get("strong") else "weak",
             "vs_baseline": None,
             "dtype": cfg["dtype"],
             "data": "synthetic (seeded; random-init probe of the paper's shape)",
             "config": {
-                "workload": f"BASELINE configs[{ {'c1': 0, 'c2': 1, 'c4': 3}[args.config] }]" +
-                            (f" / configs[2] shape at N={world}" if world > 1 else "") +
-                            ": " + cfg["desc"],
-                "n_per_gpu": cfg["n"], "waiting_per_gpu": cfg["waiting"], "d": cfg["d"],
+                "workload": workload_name(cfg_name, world),
+                "n_total": cfg["n"] * world, "n_per_gpu": cfg["n"], "waiting_per_gpu": cfg["waiting"], "d": cfg["d"],
                 "hidden": cfg["H"], "bins": cfg["k"], "c": cfg["c"],
                 "l1_kernel": {1: "gemv", 2: "tcgen05 split-K (K2c)", 3: "tcgen05 unfused", 4: "tcgen05 CTA pair (K2d)"}[mode], "l1_splits": splits,
-                "l2": "flushed between timed steps (256 MiB memset outside the step events)"
+                "l2": "flushed between timed steps, outside the step events: a 256 MiB memset "
+                      "(> the 126 MB L2) then a 256 MiB read of another buffer, so the step "
+                      "starts with none of its data in L2 and no dirty lines to write back"
                       if not args.no_flush else "warm",
                 "cuda_graph": use_graph,
                 "parallelism": f"request-sharded x{world}, replicated weights" +
@@ -456,10 +509,146 @@ def run_ours(args, cfg):
             "clocks": clk.summary(),
         }
     t.close()
+    del graphs, graphs_prof, dev, dev_init, flush
+    torch.cuda.empty_cache()
     if world > 1:
         dist.barrier()
-        dist.destroy_process_group()
     return out
+
+
+# ----------------------------------------------------------------------------- sweep
+def run_sweep(args):
+    """configs[4] (BASELINE.json): requests n = 1 ... 65 536 x c in
+    {0, 0.5, 0.8, inf}, d = 4096 bf16, k = 10, on one GPU.  Per point: the steady-state
+    predict+schedule step (n running + n/4 waiting, KV budget 0.8 x need) as CUDA graphs, L2
+    flushed between timed steps, median / p99 us per step and requests/s; the layer-1
+    kernel's HBM and tensor fractions (the regime crossover at n ~ 525); and the fp64 oracle
+    timed on a bounded sample of the same step on the host cores, all cores and one thread
+    (the cpu_baseline leg).  Parity at these points is tests/test_gpu_sweep.py."""
+    import torch
+    from paper_2410_01035_b200 import (Trail, load_library, trail_plan_l1, trail_profile_enable,
+                                       trail_profile_read)
+    load_library()
+    hbm, tf_burst, tf_sust, src = peaks()
+    device = torch.device("cuda", 0)
+    d, k = 4096, 10
+    w = W.make_weights(d, 512, k, "bf16", seed=args.seed)
+    cs = [math.inf if v == "inf" else float(v) for v in args.sweep_c.split(",")]
+    flush = L2Flush(torch, device)
+    pts = []
+    for n in [int(v) for v in args.sweep_n.split(",")]:
+        log(f"sweep n={n}")
+        eng = W.EngineScript(n, max(1, n // 4), d=d, dtype="bf16", seed=args.seed + n,
+                             burst_start=False)
+        bs = []
+        for _ in range(3):
+            bs.append(eng.batch())
+            eng.advance()
+        for c in cs:
+            t = Trail(w, c, eng.max_slots, eng.max_slots, eng.max_slots, dtype="bf16")
+            x = [dict(p=[to_dev(a, torch, device) for a in (b.emb, b.row_offsets, b.request_ids,
+                                                              b.is_prefill)],
+                      s=[to_dev(a, torch, device) for a in (b.sched_ids, b.arrival_seq,
+                                                            b.kv_blocks, b.is_running)],
+                      budget=b.kv_budget) for b in bs]
+            stream = torch.cuda.Stream(device)
+            with torch.cuda.stream(stream):
+                for b in x:
+                    t.predict(*b["p"], stream=stream)
+                    t.schedule(*b["s"], b["budget"], stream=stream)
+            torch.cuda.synchronize()
+            graphs, gprof = [], []
+            for prof in (0, 2):
+                trail_profile_enable(t.h, prof)
+                for b in x[1:]:
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=stream):
+                        t.predict(*b["p"], stream=stream)
+                        t.schedule(*b["s"], b["budget"], stream=stream)
+                    (gprof if prof else graphs).append(g)
+            trail_profile_enable(t.h, 0)
+            ms = []
+            for i in range(args.warmup + args.steps):
+                with torch.cuda.stream(stream):
+                    flush()
+                    a, bb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    graphs[i % len(graphs)].replay()
+                    bb.record(stream)
+                stream.synchronize()
+                if i >= args.warmup:
+                    ms.append(a.elapsed_time(bb))
+            kern = {}
+            trail_profile_enable(t.h, 2)
+            for i in range(10):
+                with torch.cuda.stream(stream):
+                    flush()
+                    gprof[i % len(gprof)].replay()
+                stream.synchronize()
+                for kn in ("pool", "gemv", "umma", "head", "select"):
+                    v, cn = trail_profile_read(t.h, kn)
+                    if cn:
+                        kern.setdefault(kn, []).append(v)
+            trail_profile_enable(t.h, 0)
+            kus = {kn: 1e3 * statistics.median(v) for kn, v in kern.items()}
+            mode, splits = trail_plan_l1(t.h, int(bs[1].n))
+            l1 = "gemv" if mode == 1 else "umma"
+            l1_us = kus.get(l1)
+            byts = 512 * d * 2 + bs[1].n * d * 2
+            flops = 2.0 * bs[1].n * d * 512
+            st_ = sorted(ms)
+            rec = {"n": n, "c": "inf" if math.isinf(c) else c, "records": int(bs[1].m),
+                   "us_per_step_median": 1e3 * statistics.median(ms),
+                   "us_per_step_p99": 1e3 * st_[min(len(st_) - 1, int(math.ceil(0.99 * len(st_))) - 1)],
+                   "requests_per_s": n / (statistics.median(ms) / 1e3),
+                   "kernel_us": {kk: round(v, 3) for kk, v in kus.items()},
+                   "l1_kernel": {1: "gemv", 2: "tcgen05 split-K (K2c)", 3: "tcgen05 unfused",
+                                 4: "tcgen05 CTA pair (K2d)"}[mode],
+                   "l1_bytes": byts, "l1_flops": flops,
+                   "l1_hbm_frac": (byts / (l1_us / 1e6) / 1e9 / hbm) if l1_us else None,
+                   "l1_tensor_frac_burst": (flops / (l1_us / 1e6) / 1e12 / tf_burst) if l1_us else None}
+            if c == cs[0] and not args.no_cpu:
+                cfg = dict(n=n, waiting=max(1, n // 4), d=d, H=512, k=k, dtype="bf16", c=c,
+                           total=512.0)
+                rec["cpu_baseline"] = cpu_baseline(cfg, args, min(args.cpu_seconds, 3.0),
+                                                   prebuilt=(eng, bs[0], bs[1:]))
+            pts.append(rec)
+            log(json.dumps(rec))
+            del graphs, gprof, x
+            t.close()
+            torch.cuda.empty_cache()
+    return {"sweep": "BASELINE.json configs[4] on 1 GPU: d=4096 bf16, k=10, H=512, n running + "
+                     "n/4 waiting, KV budget 0.8 x need, steady-state decode step",
+            "peaks": {"hbm_GBps": hbm, "bf16_tflops_burst": tf_burst, "source": src},
+            "l2": "flushed between timed steps (L2Flush)", "points": pts}
+
+
+def workload_name(cfg_name, world):
+    cfg = CONFIGS[cfg_name]
+    idx = {"c1": 0, "c2": 1, "c4": 3}[cfg_name]
+    extra = ""
+    if world > 1:
+        extra = (f" at N={world} (strong: {cfg['n']} requests in total)" if cfg.get("strong")
+                 else f" / configs[2] shape at N={world} ({cfg['n']} requests per GPU)")
+    return f"BASELINE configs[{idx}]{extra}: {cfg['desc']}"
+
+
+class L2Flush:
+    """Between timed steps: write a 256 MiB buffer (more than the 126 MB L2), then read a
+    second 256 MiB buffer, which evicts the written lines (their write-back happens here,
+    outside the step's events).  The step then finds none of its inputs or weights in L2 and
+    no dirty lines to write back — the state after the LLM's own layers, minus their
+    write-back, which belongs to those layers."""
+
+    def __init__(self, torch, device):
+        self.w = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+        self.r = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=device)
+        self.acc = torch.zeros((), dtype=torch.float32, device=device)
+        self.torch = torch
+
+    def __call__(self):
+        self.w.zero_()
+        self.acc = self.r.sum()
 
 
 def run_e2e(args, cfg, t, batches, stream, flush, torch, device, world):
@@ -536,7 +725,7 @@ def run_e2e(args, cfg, t, batches, stream, flush, torch, device, world):
     for i in range(steps):
         with torch.cuda.stream(stream):
             if not args.no_flush:
-                flush.zero_()
+                flush()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             h2d, d2h = step(args.warmup + i)
@@ -566,75 +755,128 @@ def _threads():
         return 1
 
 
-def oracle_steps(cfg, args, seconds: float, max_steps: int):
+def _subbatch(b, S):
+    """The first S predicted requests of a batch and the first S + S/4 scheduled records (a
+    bounded sample of the same workload for the CPU oracle; SURVEY §8(d) oracle timing)."""
+    if S is None or S >= b.n:
+        return b.emb, b.row_offsets, b.request_ids, b.is_prefill, b.sched_ids, b.arrival_seq, \
+            b.kv_blocks, b.is_running, b.kv_budget, b.n
+    ms = min(b.m, S + S // 4)
+    r1 = int(b.row_offsets[S])
+    frac = float(np.sum(b.kv_blocks[:ms])) / max(1.0, float(np.sum(b.kv_blocks)))
+    return (b.emb[:r1], b.row_offsets[:S + 1], b.request_ids[:S], b.is_prefill[:S],
+            b.sched_ids[:ms], b.arrival_seq[:ms], b.kv_blocks[:ms], b.is_running[:ms],
+            int(b.kv_budget * frac), S)
+
+
+def oracle_steps(cfg, args, seconds: float, max_steps: int, sample=None, prebuilt=None):
     from oracle import trail_ref as R
     nb = max(1, min(args.distinct, cfg.get("distinct", args.distinct), max_steps))
-    eng, init, batches = make_batches(cfg, nb, 0, 1, args.seed)
+    eng, init, batches = prebuilt if prebuilt is not None else make_batches(cfg, nb, 0, 1, args.seed)
+    nb = len(batches)
     w = W.make_weights(cfg["d"], cfg["H"], cfg["k"], cfg["dtype"],
                        edges=W.paper_bin_edges(cfg["k"], cfg["total"]), seed=args.seed)
     o = R.TrailOracle(W.decode(w["W1"], cfg["dtype"]), w["b1"], w["W2"], w["b2"], w["edges"],
                       cfg["c"], eng.max_slots, x_dtype=cfg["dtype"])
-    o.predict_step(W.decode(init.emb, cfg["dtype"]), init.row_offsets, init.request_ids,
-                   init.is_prefill)                      # burst prefill, untimed
+    e0, off0, ids0, pf0 = _subbatch(init, sample)[:4]
+    o.predict_step(W.decode(e0, cfg["dtype"]), off0, ids0, pf0)   # first observations, untimed
     cache = {}
 
-    def emb64(i):   # decoded lazily (c4: 1 GB of fp64 per batch)
+    def emb64(i, rows):   # decoded lazily (c4: 1 GB of fp64 per batch)
         if i not in cache:
             if len(cache) >= 2:
                 cache.pop(next(iter(cache)))
-            cache[i] = W.decode(batches[i].emb, cfg["dtype"])
+            cache[i] = W.decode(rows, cfg["dtype"])
         return cache[i]
     times, reqs = [], 0
     t_start = time.perf_counter()
     for s in range(max_steps):
         i = s % nb
-        b = batches[i]
+        emb, off, ids, pref, sids, arr, kv, run, budget, n = _subbatch(batches[i], sample)
+        x = emb64(i, emb)
         t0 = time.perf_counter()
-        o.predict_step(emb64(i), b.row_offsets, b.request_ids, b.is_prefill)
-        o.schedule_step(b.sched_ids, b.arrival_seq, b.kv_blocks, b.is_running, b.kv_budget)
+        o.predict_step(x, off, ids, pref)
+        o.schedule_step(sids, arr, kv, run, budget)
         times.append(time.perf_counter() - t0)
-        reqs += b.n
+        reqs += n
         if time.perf_counter() - t_start > seconds:
             break
     return times, reqs
 
 
-def cpu_baseline(cfg, args):
-    times, reqs = oracle_steps(cfg, args, seconds=args.cpu_seconds, max_steps=10_000)
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline(cfg, args, seconds, prebuilt=None):
+    """The fp64 oracle as it stands, on the host cores: all cores (BLAS threads), then one
+    thread on a shorter sample (SURVEY §8(d) oracle timing)."""
+    times, reqs = oracle_steps(cfg, args, seconds=seconds, max_steps=10_000, prebuilt=prebuilt)
     tot = sum(times)
-    return {"value": reqs / tot, "unit": "requests/s", "cores": _threads(), "kind": "oracle",
-            "ms_per_step": 1e3 * tot / len(times),
-            "sample": f"{len(times)} full steps of the same workload (numpy fp64 oracle, "
-                      f"{cfg['n']} predicted + {cfg['n'] + cfg['waiting']} scheduled requests "
-                      f"each), {tot:.1f} s of CPU work on {os.cpu_count()} host CPUs"}
+    out = {"value": reqs / tot, "unit": "requests/s", "cores": _threads(), "kind": "oracle",
+           "ms_per_step": 1e3 * tot / len(times), "cpu_model": cpu_model(),
+           "host_cpus": os.cpu_count(),
+           "sample": f"{len(times)} full steps of the same workload (numpy fp64 oracle, "
+                     f"{cfg['n']} predicted + {cfg['n'] + cfg['waiting']} scheduled requests "
+                     f"each), {tot:.1f} s of CPU work on {_threads()} BLAS threads"}
+    try:
+        from threadpoolctl import threadpool_limits
+        S = 1024 if cfg["n"] > 1024 else None
+        with threadpool_limits(limits=1):
+            t1, r1 = oracle_steps(cfg, args, seconds=seconds / 3, max_steps=10_000, sample=S,
+                                  prebuilt=prebuilt)
+        out["one_thread"] = {"value": r1 / sum(t1), "unit": "requests/s", "cores": 1,
+                             "ms_per_step": 1e3 * sum(t1) / len(t1),
+                             "sample": f"{len(t1)} steps of " + (f"the first {S} predicted + {S + S // 4} "
+                                       "scheduled requests" if S else "the full workload") +
+                                       f", {sum(t1):.1f} s"}
+    except Exception as e:   # noqa: BLE001 (report, do not fail the bench)
+        out["one_thread"] = {"unavailable": str(e)}
+    return out
 
 
-def run_reference(args, cfg):
+def run_reference(args):
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     if rank != 0:
         return None
-    times, reqs = oracle_steps(cfg, args, seconds=1e9, max_steps=args.warmup + args.steps)
+    cfg = CONFIGS[args.config]
+    # each reference step is a bounded sample of the workload (<= 512 predicted requests), and
+    # the run stops after ~150 s of oracle work whatever K is (steps actually timed reported)
+    S = 512 if cfg["n"] > 512 else None
+    times, reqs = oracle_steps(cfg, args, seconds=150.0, max_steps=args.warmup + args.steps,
+                               sample=S)
+    per_step = min(S, cfg["n"]) if S else cfg["n"]
     times = times[args.warmup:] if len(times) > args.warmup else times
     n_steps = len(times)
     tot = sum(times)
     ms = 1e3 * tot / n_steps
-    val = cfg["n"] / (ms / 1e3)
+    val = per_step / (ms / 1e3)
     return {
         "impl": "reference",
         "metric": "predict+schedule requests/s", "value": val, "unit": "requests/s",
         "n_gpus": world, "steps": n_steps, "warmup": args.warmup, "ms_per_step": ms,
-        "us_per_iteration": ms * 1e3, "higher_is_better": True, "scaling": "weak",
+        "us_per_iteration": ms * 1e3, "higher_is_better": True,
+        "scaling": "strong" if cfg.get("strong") else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
-        "config": {"workload": f"BASELINE configs[{ {'c1': 0, 'c2': 1, 'c4': 3}[args.config] }]" +
-                               (f" / configs[2] shape at N={world}" if world > 1 else "") +
-                               ": " + cfg["desc"],
-                   "n_per_gpu": cfg["n"], "waiting_per_gpu": cfg["waiting"], "d": cfg["d"],
+        "config": {"workload": workload_name(args.config, world),
+                   "n_total": cfg["n"] * (1 if cfg.get("strong") else world), "n_per_gpu": cfg["n"], "waiting_per_gpu": cfg["waiting"], "d": cfg["d"],
                    "hidden": cfg["H"], "bins": cfg["k"], "c": cfg["c"],
                    "note": "the fp64 CPU oracle (oracle/trail_ref.py) is the reference arm: the "
                            "paper ships no code"},
         "cpu_baseline": {"value": val, "unit": "requests/s", "cores": _threads(), "kind": "oracle",
-                         "sample": f"{n_steps} full steps, rank 0 only"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"{n_steps} timed steps of " +
+                                   (f"the first {S} predicted + {S + S // 4} scheduled requests "
+                                    "of each iteration" if S else "the full workload") +
+                                   ", rank 0 only"},
         "e2e": {"value": val, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -645,10 +887,17 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS),
+                    help="headline workload (default configs[3], the largest single-GPU config)")
+    ap.add_argument("--sub", default="c2,c1",
+                    help="comma list of further configs reported as sub-records of the line")
     ap.add_argument("--distinct", type=int, default=16, help="distinct iterations cycled")
     ap.add_argument("--seed", type=int, default=W.MASTER_SEED)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--sweep", action="store_true", help="configs[4] sweep instead of one line")
+    ap.add_argument("--sweep-n", default="1,4,16,64,256,512,1024,2048,4096,16384,65536")
+    ap.add_argument("--sweep-c", default="0,0.5,0.8,inf")
+    ap.add_argument("--sweep-out", default=os.path.join(ROOT, "profiles", "r02_sweep.json"))
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -656,10 +905,30 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    cfg = CONFIGS[args.config]
-    out = run_reference(args, cfg) if args.impl == "reference" else run_ours(args, cfg)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch(args.gpus)
+        return
+    if args.sweep:
+        doc = run_sweep(args)
+        with open(args.sweep_out, "w") as f:
+            json.dump(doc, f, indent=1)
+        log(f"sweep written to {args.sweep_out}")
+        return
+    out = run_reference(args) if args.impl == "reference" else run_ours(args)
     if out is not None:
         print(json.dumps(out), flush=True)
+
+
+def relaunch(n):
+    """`python bench.py --gpus N` without torchrun: re-exec under torch.distributed.run with
+    N local ranks (127.0.0.1 rendezvous), so the N-GPU line is always measured with N ranks."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
 
 
 if __name__ == "__main__":

@@ -133,6 +133,29 @@ TRAIL_API trail_status trail_predict_step(trail_handle h, const void *emb, int64
                                 int32_t n, float *posteriors, float *expected_remaining,
                                 trail_stream stream);
 
+/* Multi-layer weighted embeddings ("estimate the prediction using
+ * ... a weighted average of their outputs", "leveraging multiple-layer embeddings
+ * through weighted averaging"; reading D-28).  The probe input of request j is
+ *   u_j = sum_l a_l u_{l,j},   a = layer_weights / sum(layer_weights),
+ * u_{l,j} = layer l's embedding of request j: the mean of its prompt rows at prefill,
+ * its row at decode.  Every layer buffer uses the same row_offsets and emb_ld.  The weighted
+ * mean is accumulated in fp32 (layer order, rows in order), divided by the row count
+ * (correctly rounded), rounded to bf16 (RNE) once for bf16 handles (D-12), written to a
+ * library buffer [max_requests][d] (allocated on first use: synchronising, so make the
+ * first call outside CUDA-graph capture), and the rest of the step is trail_predict_step
+ * on it (one row per request; is_prefill keeps its meaning).
+ *   embs           (host) array of n_layers DEVICE pointers, [rows][emb_ld] cfg.dtype each
+ *   layer_weights  (host) n_layers finite non-negative fp32 with a positive sum
+ *   n_layers       1 .. 8
+ * Other arguments, outputs and errors as trail_predict_step; TRAIL_ERR_INVALID for bad
+ * weights or n_layers. */
+TRAIL_API trail_status trail_predict_step_layers(trail_handle h, const void *const *embs,
+                                const float *layer_weights, int32_t n_layers, int64_t emb_ld,
+                                const int32_t *row_offsets, const uint32_t *request_ids,
+                                const uint8_t *is_prefill, const float *prior_override,
+                                int32_t n, float *posteriors, float *expected_remaining,
+                                trail_stream stream);
+
 /* Chunked prefill (P:432 vLLM chunked prefill, reading D-27).  A prompt's
  * rows may arrive over several iterations; the pooled input is still the mean of ALL its
  * rows.  For each of the n requests, adds its chunk's rows
@@ -192,15 +215,21 @@ TRAIL_API trail_status trail_schedule_step(trail_handle h, const uint32_t *reque
                                  int32_t max_run, uint32_t *run_ids, uint32_t *preempt_ids,
                                  uint32_t *admit_ids, int32_t *counts, trail_stream stream);
 
-/* The two halves of trail_schedule_step, for callers that run their own collective.
- * pack writes n 16-byte records {u32 keybits, u32 arrival_seq, u32 kv_blocks,
- * u32 (id_base+slot) | running<<31} where keybits = (!forced)<<31 | fp32 bits of the key.
+/* The two halves of trail_schedule_step, for callers that run their own collective
+ * (SURVEY §8(b) prose alternative: pack -> caller's all-gather -> select).
+ * pack writes `capacity` (>= n) 16-byte records {u32 keybits, u32 arrival_seq,
+ * u32 kv_blocks, u32 (id_base+slot) | running<<31} where keybits = (!forced)<<31 | fp32 bits
+ * of the key (P:394 forced = rank -inf, P:570 key = predicted remaining length); records
+ * [n, capacity) are padding (keybits = arrival = id word = 0xFFFFFFFF, kv = 0) so that every rank sends the same byte
+ * count — this is the same kernel, with capacity = max_sched, that trail_schedule_step
+ * runs before its NCCL all-gather.  `records` is device memory of capacity * 16 bytes.
  * select consumes n_records such records (from any number of ranks, any order; records
- * with keybits == 0xFFFFFFFF are padding and ignored). */
+ * with keybits == 0xFFFFFFFF are padding and ignored); n_records <= max_sched * world_size.
+ * Errors: TRAIL_ERR_INVALID for capacity < n or NULL pointers. */
 TRAIL_API trail_status trail_schedule_pack(trail_handle h, const uint32_t *request_ids,
                                  const uint32_t *arrival_seq, const int32_t *kv_blocks,
-                                 const uint8_t *is_running, int32_t n, void *records,
-                                 trail_stream stream);
+                                 const uint8_t *is_running, int32_t n, int32_t capacity,
+                                 void *records, trail_stream stream);
 TRAIL_API trail_status trail_schedule_select(trail_handle h, const void *records, int32_t n_records,
                                    int64_t kv_budget, int32_t max_run, uint32_t *run_ids,
                                    uint32_t *preempt_ids, uint32_t *admit_ids,
@@ -264,6 +293,24 @@ TRAIL_API trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode);
  * (predict step or time update) and stored as the slot threshold.  Synchronising; CUDA
  * graphs captured earlier keep the old rule.  Errors: TRAIL_ERR_INVALID (mode not 0/1). */
 TRAIL_API trail_status trail_set_threshold_mode(trail_handle h, int32_t mode);
+
+/* Budget fill rule of the selection (row a6; P:171 is silent, reading D-15).  0 (default):
+ * strict prefix — stop at the first request in priority order whose KV blocks do not fit.
+ * 1: first-fit — skip it and keep taking every later request that still
+ * fits the remaining budget and run cap; the lists stay in priority order.  Applies to
+ * trail_schedule_step / trail_schedule_select calls enqueued afterwards (CUDA graphs captured
+ * earlier keep the old rule).  Errors: TRAIL_ERR_INVALID (mode not 0/1). */
+TRAIL_API trail_status trail_set_fill_mode(trail_handle h, int32_t mode);
+
+/* L2-persisting W1 (optional; W1 is 99.7 % of the probe's parameters).
+ * 1: sets the device's persisting-L2 set-aside to cover W1 (cudaLimitPersistingL2CacheSize —
+ * a DEVICE-WIDE limit) and attaches an access-policy window (persisting hits, streaming misses)
+ * over the library's W1 copy to every layer-1 launch, so W1 survives the LLM layers that run
+ * between two predict steps.  0 (default): normal caching; resets the persisting lines and
+ * the set-aside.  Launches enqueued afterwards follow the setting (graphs captured earlier
+ * keep theirs).  Errors: TRAIL_ERR_UNSUPPORTED if the device has no persisting L2,
+ * TRAIL_ERR_CUDA. */
+TRAIL_API trail_status trail_set_w1_l2_persist(trail_handle h, int32_t enable);
 
 /* Optional host-side hint: the number of embedding rows (the flat batch's token count,
  * row_offsets[n] - row_offsets[0]) of the next trail_predict_step calls; 0 = unknown (the

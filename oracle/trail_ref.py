@@ -234,12 +234,45 @@ class TrailOracle:
         """p^(t) = softmax(MLP(u^(t))) (a2 + first half of a3)."""
         return softmax(classifier_logits(X, self.W1, self.b1, self.W2, self.b2))
 
+    def mixed_inputs(self, embs, row_offsets: np.ndarray, layer_weights) -> np.ndarray:
+        """Multi-layer weighted embeddings (P:194 'estimate the prediction using ... a
+        weighted average of their outputs'; P:717 'leveraging multiple-layer embeddings
+        through weighted averaging', reading D-28): the probe input of
+        request j is u_j = sum_l a_l u_{l,j} with a = w / sum(w), where u_{l,j} is layer l's
+        embedding of request j (its prompt mean at prefill; its row at decode).  Each
+        layer is pooled in fp64, the weighted sum is fp64, and bf16 inputs are rounded to
+        bf16 once, at the end (D-12)."""
+        w = np.asarray(layer_weights, dtype=np.float64)
+        a = w / w.sum()
+        off = np.asarray(row_offsets, np.int64)
+        n = off.shape[0] - 1
+        X = np.zeros((n, np.asarray(embs[0]).shape[1]), dtype=np.float64)
+        for j in range(n):
+            for al, e in zip(a, embs):
+                X[j] += al * np.asarray(e[off[j]:off[j + 1]], dtype=np.float64).mean(axis=0)
+        return bf16_round(X) if self.x_dtype == "bf16" else X
+
+    def predict_step_layers(self, embs, row_offsets: np.ndarray, request_ids: np.ndarray,
+                            is_prefill: np.ndarray, layer_weights,
+                            prior_override: Optional[np.ndarray] = None
+                            ) -> Tuple[np.ndarray, np.ndarray]:
+        """predict_step on the weighted average of several layers' embeddings (D-28)."""
+        return self.predict_from_inputs(self.mixed_inputs(embs, row_offsets, layer_weights),
+                                        request_ids, is_prefill, prior_override)
+
     def predict_step(self, emb: np.ndarray, row_offsets: np.ndarray, request_ids: np.ndarray,
                      is_prefill: np.ndarray, prior_override: Optional[np.ndarray] = None
                      ) -> Tuple[np.ndarray, np.ndarray]:
         """One iteration for the n requests that just ran.  emb: fp64 values [R, d]."""
+        return self.predict_from_inputs(self.pooled_inputs(emb, np.asarray(row_offsets, np.int64)),
+                                        request_ids, is_prefill, prior_override)
+
+    def predict_from_inputs(self, X: np.ndarray, request_ids: np.ndarray, is_prefill: np.ndarray,
+                            prior_override: Optional[np.ndarray] = None
+                            ) -> Tuple[np.ndarray, np.ndarray]:
+        """The classifier, softmax, Bayes step and L for given probe inputs X [n, d]."""
         ids = np.asarray(request_ids, dtype=np.int64)
-        p = self.probs(self.pooled_inputs(emb, np.asarray(row_offsets, np.int64)))
+        p = self.probs(X)
         st = self.state
         first = (np.asarray(is_prefill) != 0) | ~st.seen[ids]
         q = np.empty_like(p)
@@ -297,10 +330,10 @@ class TrailOracle:
         return key, forced
 
     def schedule_step(self, ids, arrival_seq, kv_blocks, is_running, kv_budget: int,
-                      max_run: int = 0, id_base: int = 0):
+                      max_run: int = 0, id_base: int = 0, fill: str = "prefix"):
         key, forced = self.keys_and_forced(ids, is_running)
         return select(key, forced, arrival_seq, kv_blocks, is_running,
-                      np.asarray(ids, dtype=np.int64) + id_base, kv_budget, max_run)
+                      np.asarray(ids, dtype=np.int64) + id_base, kv_budget, max_run, fill)
 
     def release(self, ids) -> None:
         """A finished (or aborted) request frees its slot: the slot is unseen again and any
@@ -311,15 +344,17 @@ class TrailOracle:
 
 
 def select(key, forced, arrival_seq, kv_blocks, is_running, ids, kv_budget: int,
-           max_run: int = 0):
+           max_run: int = 0, fill: str = "prefix"):
     """Limited-preemption SPRPT over running + waiting requests.
 
     Order: forced (rank -inf) first, then ascending predicted remaining length, ties by
     arrival (FCFS; D-18), then input position (stable).  Run set = every forced
     request plus the longest prefix of the rest whose cumulative KV blocks, added to the
     forced total, stays within the budget (and whose size stays within max_run if > 0);
-    stop at the first request that does not fit (D-15).  If the forced set alone violates
-    a limit the run set is the forced set and the status is WARN_OVER_BUDGET (D-16).
+    stop at the first request that does not fit (D-15).  fill='first_fit' (SURVEY §8(f)3,
+    the D-15 alternative): walk the whole order and take every request that still fits,
+    skipping the ones that do not.  If the forced set alone violates a limit the run set is
+    the forced set and the status is WARN_OVER_BUDGET (D-16).
     Returns (run_ids, preempt_ids, admit_ids, status), lists in sorted order."""
     key = np.asarray(key, dtype=np.float64)
     forced = np.asarray(forced, dtype=bool)
@@ -346,7 +381,18 @@ def select(key, forced, arrival_seq, kv_blocks, is_running, ids, kv_budget: int,
             n_run += 1
     in_run = np.zeros(m, dtype=bool)
     in_run[order[:n_run]] = True
-    run = [ids[j] for j in order[:n_run]]
+    if fill == "first_fit" and status == STATUS_OK:
+        for pos in range(n_run, m):
+            j = order[pos]
+            if n_run + 1 > cap:
+                break
+            if used + kv[j] <= kv_budget:
+                used += kv[j]
+                n_run += 1
+                in_run[j] = True
+    elif fill not in ("prefix", "first_fit"):
+        raise ValueError(fill)
+    run = [ids[j] for j in order if in_run[j]]
     preempt = [ids[j] for j in order if running[j] and not in_run[j]]
     admit = [ids[j] for j in order if (not running[j]) and in_run[j]]
     return (np.array(run, dtype=np.int64), np.array(preempt, dtype=np.int64),

@@ -19,6 +19,7 @@ from .trail import (  # noqa: F401
     trail_nccl_unique_id,
     trail_plan_l1,
     trail_predict_step,
+    trail_predict_step_layers,
     trail_profile_enable,
     trail_profile_read,
     trail_read_state,
@@ -26,7 +27,9 @@ from .trail import (  # noqa: F401
     trail_schedule_pack,
     trail_schedule_select,
     trail_schedule_step,
+    trail_set_fill_mode,
     trail_set_l1_mode,
+    trail_set_w1_l2_persist,
     trail_trace_enable,
     trail_trace_read,
 )

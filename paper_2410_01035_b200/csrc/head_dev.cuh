@@ -64,23 +64,23 @@ __device__ __forceinline__ void head_seg(int j, int n, int k, int SEG, int b, fl
     }
     lq = lpr + lp;
   }
-  // (max, argmax) of the unnormalised log q, lowest index on ties (argmax of q^(0), D-9)
-  float qmax = lq;
-  int bi = act ? b : 0x7FFFFFFF;
+  // (max, argmax) of the unnormalised log q, lowest index on ties (argmax of q^(0), D-9), and
+  // of log p for the D-5 fallback — reduced together by every lane (no divergent shuffles:
+  // inactive segments also have an all -inf q)
+  float qmax = lq, pmax = act ? lp : -INFINITY;
+  int bi = act ? b : 0x7FFFFFFF, pi = bi;
   for (int o = SEG >> 1; o > 0; o >>= 1) {
     const float ov = __shfl_xor_sync(0xffffffffu, qmax, o, SEG);
     const int oi = __shfl_xor_sync(0xffffffffu, bi, o, SEG);
+    const float pv = __shfl_xor_sync(0xffffffffu, pmax, o, SEG);
+    const int pj = __shfl_xor_sync(0xffffffffu, pi, o, SEG);
     if (ov > qmax || (ov == qmax && oi < bi)) { qmax = ov; bi = oi; }
+    if (pv > pmax || (pv == pmax && pj < pi)) { pmax = pv; pi = pj; }
   }
   if (qmax == -INFINITY) {          // all-zero product: fall back to p (D-5); only reachable
-    lq = lp;                        // for a prior that is zero on every bin.  The argmax is
-    qmax = lq;                      // redone over p, as K3 and the oracle do.
-    bi = act ? b : 0x7FFFFFFF;
-    for (int o = SEG >> 1; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, qmax, o, SEG);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o, SEG);
-      if (ov > qmax || (ov == qmax && oi < bi)) { qmax = ov; bi = oi; }
-    }
+    lq = lp;                        // for a prior that is zero on every bin; the threshold
+    qmax = pmax;                    // comes from argmax p, as in K3 and the oracle
+    bi = pi;
   }
   const float qs = seg_sum(act ? __expf(lq - qmax) : 0.f, SEG);   // every lane shuffles
   lq = act ? lq - (qmax + __logf(qs)) : -INFINITY;

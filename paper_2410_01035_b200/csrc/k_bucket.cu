@@ -13,11 +13,13 @@
 //   B1  histogram of (count, KV, running) per bucket (warp-aggregated global atomics)
 //   B2  scatter of the records into bucket order (prefix of the counts, atomic cursors)
 //   B3  each record counts the records of its own bucket ordered before it (the bucket range
-//       is staged in shared memory; 8 threads per record), adds the bucket prefixes
+//       is staged in shared memory; 16 threads per record, so a tie cluster of b records is
+//       spread over b/64 CTAs with b/16 compares per thread), adds the bucket prefixes
 //       -> position, cumulative KV, running-before, and the lists follow as in k_rank.cu
 //       (one packed acq_rel atomic; the last CTA writes the preempt list and re-arms).
-// Cost is O(m + sum over buckets of size^2 / 8); a tie cluster (e.g. never-observed requests,
-// all keyed E_pi[L]) is spread over the CTAs that own its positions.
+// Cost is O(m + sum over buckets of size^2 / 16); a tie cluster (e.g. never-observed requests,
+// all keyed E_pi[L]) is spread over the CTAs that own its positions.  Equal (key, arrival)
+// pairs are ordered by input position, as in the oracle's stable sort (D-18).
 #include <algorithm>
 
 #include "trail_internal.cuh"
@@ -28,13 +30,14 @@ namespace {
 constexpr int kBH = 1024;               // buckets per class (forced / not forced)
 constexpr int kB = 2 * kBH;
 constexpr int kB3Threads = 1024;
-constexpr int kB3Items = kB3Threads / 8;
+constexpr int kB3Tpi = 16;             // threads per record in B3
+constexpr int kB3Items = kB3Threads / kB3Tpi;
 constexpr int kStageCap = 8192;         // bucket entries staged in shared memory (128 KB)
 
 struct BkEntry {                        // bucket-sorted record (16 B)
   unsigned long long key;               // keybits << 32 | arrival
-  uint32_t kv;
-  uint32_t gid;                         // (id_base + slot) | running << 31
+  uint32_t kvr;                         // kv | running << 31  (kv_blocks >= 0 fits 31 bits)
+  uint32_t idx;                         // input position (final tie-break, D-18)
 };
 
 __device__ __forceinline__ int bk_bucket(uint32_t keybits, float m0, float scale) {
@@ -47,7 +50,7 @@ __device__ __forceinline__ int bk_bucket(uint32_t keybits, float m0, float scale
 }
 
 __device__ __forceinline__ bool bk_less(const BkEntry &a, const BkEntry &b) {
-  return a.key < b.key || (a.key == b.key && (a.gid & 0x7FFFFFFFu) < (b.gid & 0x7FFFFFFFu));
+  return a.key < b.key || (a.key == b.key && a.idx < b.idx);
 }
 
 // exclusive scan of kB (u32 count, u32 run, u64 kv) bucket totals by a 1024-thread CTA
@@ -100,10 +103,15 @@ __device__ void bk_scan_buckets(BkScan &sh, const uint32_t *hcnt, const uint32_t
 
 // B1: per-bucket totals
 __global__ void __launch_bounds__(256)
-trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, float m0, float scale,
+trail_bucket_hist_kernel(const Record *__restrict__ rec, Record *__restrict__ rec_out,
+                         const uint32_t *__restrict__ ids, const uint32_t *__restrict__ arrival,
+                         const int32_t *__restrict__ kvin, const uint8_t *__restrict__ running,
+                         const SlotMeta *__restrict__ meta, const HeadConsts *__restrict__ cst,
+                         int max_slots, uint32_t id_base, uint32_t *__restrict__ err,
+                         int m, float m0, float scale,
                          uint32_t *__restrict__ hcnt, uint32_t *__restrict__ hrun,
                          unsigned long long *__restrict__ hkv) {
-  griddep_wait();     // records from the pack kernel / the all-gather
+  griddep_wait();     // records from the pack kernel / the all-gather, or the slot state
   griddep_launch();
   const int lane = threadIdx.x & 31;
   for (int i0 = blockIdx.x * blockDim.x; i0 < m; i0 += gridDim.x * blockDim.x) {
@@ -111,7 +119,15 @@ trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, float m0, float 
     int b = -1;
     uint32_t kvv = 0, runn = 0;
     if (i < m) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4 *>(rec + i));
+      uint4 v;
+      if (rec) {
+        v = __ldg(reinterpret_cast<const uint4 *>(rec + i));
+      } else {        // local path: row a4 fused (the record build of trail_schedule_pack)
+        const Record r = build_record(__ldg(ids + i), __ldg(arrival + i), __ldg(kvin + i),
+                                      __ldg(running + i) != 0, meta, cst, max_slots, id_base, err);
+        rec_out[i] = r;
+        v = make_uint4(r.keybits, r.arrival, r.kv, r.gid);
+      }
       if (v.x != kPadKey) {
         b = bk_bucket(v.x, m0, scale);
         kvv = v.z;
@@ -160,8 +176,8 @@ trail_bucket_scatter_kernel(const Record *__restrict__ rec, int m, float m0, flo
       const uint32_t slot = sh.cnt[b] + base + __popc(peers & ((1u << lane) - 1u));
       BkEntry e;
       e.key = ((unsigned long long)v.x << 32) | v.y;
-      e.kv = v.z;
-      e.gid = v.w;
+      e.kvr = (v.z & 0x7FFFFFFFu) | (v.w & 0x80000000u);
+      e.idx = (uint32_t)i;
       sorted[slot] = e;
     }
   }
@@ -169,7 +185,8 @@ trail_bucket_scatter_kernel(const Record *__restrict__ rec, int m, float m0, flo
 
 // B3: exact positions, cumulative KV, running-before; lists
 __global__ void __launch_bounds__(kB3Threads)
-trail_bucket_rank_kernel(int m, float m0, float scale, uint32_t *__restrict__ hcnt,
+trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, float m0, float scale,
+                         uint32_t *__restrict__ hcnt,
                          uint32_t *__restrict__ hrun, unsigned long long *__restrict__ hkv,
                          uint32_t *__restrict__ cursor, const BkEntry *__restrict__ sorted,
                          long long budget, int max_run, unsigned long long *__restrict__ gcnt,
@@ -216,8 +233,8 @@ trail_bucket_rank_kernel(int m, float m0, float scale, uint32_t *__restrict__ hc
   if (staged)
     for (int q = lo + t; q < hi; q += kB3Threads) stage[q - lo] = sorted[q];
   __syncthreads();
-  // 8 threads per record
-  const int li = t >> 3, part = t & 7;
+  // kB3Tpi threads per record
+  const int li = t / kB3Tpi, part = t % kB3Tpi;
   const int p = p0 + li;
   const bool have = p < p1;
   BkEntry me;
@@ -231,32 +248,33 @@ trail_bucket_rank_kernel(int m, float m0, float scale, uint32_t *__restrict__ hc
   uint32_t cnt = 0, rb = 0;
   unsigned long long cum = 0;
   if (have) {
-    for (int q = bs + part; q < be; q += 8) {
+    for (int q = bs + part; q < be; q += kB3Tpi) {
       const BkEntry o = staged ? stage[q - lo] : sorted[q];
-      if (bk_less(o, me)) { ++cnt; cum += o.kv; rb += o.gid >> 31; }
+      if (bk_less(o, me)) { ++cnt; cum += o.kvr & 0x7FFFFFFFu; rb += o.kvr >> 31; }
     }
   }
 #pragma unroll
-  for (int o = 1; o < 8; o <<= 1) {
+  for (int o = 1; o < kB3Tpi; o <<= 1) {
     cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     rb += __shfl_xor_sync(0xffffffffu, rb, o);
     cum += __shfl_xor_sync(0xffffffffu, cum, o);
   }
   if (have && part == 0) {
     const int pos = (int)(sh.cnt[b] + cnt);
-    const unsigned long long cum_incl = sh.kv[b] + cum + me.kv;
+    const unsigned long long cum_incl = sh.kv[b] + cum + (me.kvr & 0x7FFFFFFFu);
     const uint32_t rbefore = sh.run[b] + rb;
     const bool forced = (me.key >> 63) == 0ull;
-    const bool runn = (me.gid >> 31) != 0u;
+    const bool runn = (me.kvr >> 31) != 0u;
     const bool in_run = forced ? true : (!over && (long long)cum_incl <= budget && pos < cap);
-    const uint32_t gid = me.gid & 0x7FFFFFFFu;
+    const uint32_t gidw = __ldg(&rec[me.idx].gid);
+    const uint32_t gid = gidw & 0x7FFFFFFFu;
     if (in_run) {
       run_ids[pos] = gid;
       if (!runn) adm_ids[pos - (int)rbefore] = gid;
       atomicAdd(&s_run, 1u);
       if (runn) atomicAdd(&s_rcut, 1u);
     }
-    scratch[pos] = make_uint2(me.gid, rbefore);
+    scratch[pos] = make_uint2(gidw, rbefore);
   }
   __syncthreads();
   if (t == 0) {
@@ -299,9 +317,12 @@ cudaError_t select_bucket_prepare() {
                               (int)(sizeof(BkScan) + kStageCap * sizeof(BkEntry)));
 }
 
-cudaError_t launch_select_bucket(const Ctx &c, const Record *rec, int m, int64_t budget,
+cudaError_t launch_select_bucket(const Ctx &c, const Record *rec_in, Record *rec_out,
+                                 const uint32_t *ids, const uint32_t *arrival, const int32_t *kv,
+                                 const uint8_t *running, int m, int64_t budget,
                                  int max_run, uint32_t *run, uint32_t *pre, uint32_t *adm,
                                  int32_t *counts, cudaStream_t s) {
+  const Record *rec = rec_in ? rec_in : rec_out;
   if (!c.bk_ws) return cudaErrorInvalidValue;
   uint8_t *ws = reinterpret_cast<uint8_t *>(c.bk_ws);
   unsigned long long *hkv = reinterpret_cast<unsigned long long *>(ws);
@@ -315,8 +336,10 @@ cudaError_t launch_select_bucket(const Ctx &c, const Record *rec, int m, int64_t
   const float m0 = hc.m[0], mk = hc.m[c.k - 1];
   const float scale = mk > m0 ? (float)kBH / (mk - m0) : 0.f;
   const int g1 = std::max(1, std::min(2 * c.num_sms, (m + 255) / 256));
-  cudaError_t e = launch_k(trail_bucket_hist_kernel, dim3(g1), dim3(256), 0, s, rec, m, m0, scale,
-                           hcnt, hrun, hkv);
+  cudaError_t e = launch_k(trail_bucket_hist_kernel, dim3(g1), dim3(256), 0, s, rec_in, rec_out,
+                           ids, arrival, kv, running, (const SlotMeta *)c.meta,
+                           (const HeadConsts *)c.consts, c.cfg.max_slots, c.cfg.id_base,
+                           c.dev_err, m, m0, scale, hcnt, hrun, hkv);
   if (e != cudaSuccess) return e;
   const int g2 = std::max(1, std::min(c.num_sms, (m + kB3Threads - 1) / kB3Threads));
   e = launch_k(trail_bucket_scatter_kernel, dim3(g2), dim3(kB3Threads), sizeof(BkScan), s, rec, m,
@@ -325,7 +348,7 @@ cudaError_t launch_select_bucket(const Ctx &c, const Record *rec, int m, int64_t
   if (e != cudaSuccess) return e;
   const int g3 = std::max(1, (m + kB3Items - 1) / kB3Items);
   return launch_k(trail_bucket_rank_kernel, dim3(g3), dim3(kB3Threads),
-                  sizeof(BkScan) + kStageCap * sizeof(BkEntry), s, m, m0, scale, hcnt, hrun, hkv,
+                  sizeof(BkScan) + kStageCap * sizeof(BkEntry), s, rec, m, m0, scale, hcnt, hrun, hkv,
                   cursor, (const BkEntry *)sorted, (long long)budget, max_run, gcnt, scratch, run,
                   pre, adm, counts);
 }

@@ -532,7 +532,7 @@ cudaError_t launch_fused_predict(Ctx &c, const void *emb, int64_t ld, const int3
   cfg.gridDim = dim3((n + BM - 1) / BM, c.H / BN, splits);
   cfg.blockDim = dim3(THREADS);
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   int na = 0;
   attr[na].id = cudaLaunchAttributeClusterDimension;
   attr[na].val.clusterDim.x = 1;
@@ -544,14 +544,24 @@ cudaError_t launch_fused_predict(Ctx &c, const void *emb, int64_t ld, const int3
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
+  na = add_l1_window(attr, na);
   cfg.attrs = attr;
   cfg.numAttrs = na;
   uint64_t *trace =
       (c.trace && (int)(cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z) <= c.trace_cap) ? c.trace
                                                                                        : nullptr;
-  // the spin-wait head needs every cluster resident at once (one wave)
+  // the spin-wait head needs every cluster resident at once.  Occupancy on an idle GPU says
+  // one wave fits, but nothing guarantees it under MPS / green contexts / a concurrent
+  // persistent kernel (the side-stream overlap use case), where a spinning CTA could wait on
+  // a peer that never gets an SM.  So the default is the last-arriver head (no inter-CTA
+  // wait); TRAIL_HEAD_SPIN=1 opts into the spin head for a GPU the caller owns exclusively.
   const int tiles = (int)(cfg.gridDim.x * cfg.gridDim.y);
-  const int spin = (splits <= MAXS && tiles <= c.fused_max_clusters[splits] && !getenv("TRAIL_HEAD_LAST")) ? 1 : 0;
+  static const bool spin_opt_in = [] {
+    const char *e = getenv("TRAIL_HEAD_SPIN");
+    return e && e[0] == '1';
+  }();
+  const int spin =
+      (spin_opt_in && splits <= MAXS && tiles <= c.fused_max_clusters[splits]) ? 1 : 0;
 #define TRAIL_FUSED(KB)                                                                          \
   cfg.dynamicSmemBytes = FCfg<KB>::SMEM_TOTAL;                                                     \
   return cudaLaunchKernelEx(&cfg, trail_fused_predict_kernel<KB>, c.tmap_emb, c.tmap_emb4,       \

@@ -304,7 +304,7 @@ cudaError_t launch_wide_predict(Ctx &c, const void *emb, int64_t ld, const int32
   cfg.gridDim = dim3(2 * ((n + 2 * WBM - 1) / (2 * WBM)));
   cfg.blockDim = dim3(WT);
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   int na = 0;
   attr[na].id = cudaLaunchAttributeClusterDimension;
   attr[na].val.clusterDim.x = 2;
@@ -316,6 +316,7 @@ cudaError_t launch_wide_predict(Ctx &c, const void *emb, int64_t ld, const int32
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
+  na = add_l1_window(attr, na);
   cfg.attrs = attr;
   cfg.numAttrs = na;
 #define TRAIL_WIDE(KB)                                                                            \

@@ -9,6 +9,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
+#include <vector>
 #include <new>
 
 #include "trail_internal.cuh"
@@ -146,9 +148,9 @@ trail_status set_device(const Ctx &c) {
 
 void free_ctx(Ctx &c) {
   void *ptrs[] = {c.w1, c.b1, c.w2, c.b2, c.consts, c.lq, c.meta, c.dev_err, c.xs,
-                  c.partial, c.rec_local, c.rec_all, c.sel_scratch, c.zpart, c.arrive_cnt, c.trace,
+                  c.partial, c.rec_local, c.rec_all, c.zpart, c.arrive_cnt, c.trace,
                   c.rank_sorted, c.rank_cnt, c.pool_head, c.pool_tail, c.pool_cnt, c.bk_ws,
-                  c.chunk_acc, c.chunk_cnt};
+                  c.chunk_acc, c.chunk_cnt, c.xmix, c.iota};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   if (c.prof_ev) {
@@ -216,7 +218,9 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
   if (g.world_size < 1) return TRAIL_ERR_INVALID;
   if (g.l1_mode < 0 || g.l1_mode > 4) return TRAIL_ERR_INVALID;
   if (g.l1_mode >= TRAIL_L1_UMMA && g.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
-  if ((int64_t)g.max_sched * g.world_size > (1 << 26)) return TRAIL_ERR_INVALID;
+  // every selection runs in one thread-block cluster: 16 x 8192 records (8 x 8192 where a
+  // 16-CTA cluster cannot be resident; checked again after select_prepare)
+  if ((int64_t)g.max_sched * g.world_size > 16 * 8192) return TRAIL_ERR_CAPACITY;
   const int k = g.k;
   const double *e = g.bin_edges;
   if (!(e[0] >= 0.0)) return TRAIL_ERR_INVALID;
@@ -306,15 +310,13 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
   ALLOC(c.pool_cnt, (size_t)g.max_requests * sizeof(uint32_t));
   if (cudaMemset(c.pool_cnt, 0, (size_t)g.max_requests * sizeof(uint32_t)) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
-  ALLOC(c.rank_sorted, (size_t)max_sched * c.world * sizeof(Record));
+  ALLOC(c.rank_sorted, (size_t)std::min(max_sched * c.world, kRankMaxRecords) * sizeof(Record));
+  ALLOC(c.rank_cnt, 16 * sizeof(uint32_t));
+  if (cudaMemset(c.rank_cnt, 0, 16 * sizeof(uint32_t)) != cudaSuccess) return fail(TRAIL_ERR_CUDA);
   c.bk_cap = max_sched * c.world;
   ALLOC(c.bk_ws, bucket_workspace_bytes(c.bk_cap));
   if (cudaMemset(c.bk_ws, 0, bucket_workspace_bytes(c.bk_cap)) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
-  ALLOC(c.rank_cnt, 16 * sizeof(uint32_t));
-  if (cudaMemset(c.rank_cnt, 0, 16 * sizeof(uint32_t)) != cudaSuccess) return fail(TRAIL_ERR_CUDA);
-  c.sel_scratch_bytes = select_scratch_bytes(max_sched * c.world);
-  if (c.sel_scratch_bytes) ALLOC(c.sel_scratch, c.sel_scratch_bytes);
   const size_t m_tiles = ((size_t)g.max_requests + 127) / 128;
   if (c.dtype == TRAIL_BF16) {
     ALLOC(c.zpart, (size_t)g.max_requests * (c.H / 128) * k * sizeof(float));
@@ -338,6 +340,7 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
       fused_prepare(c) != cudaSuccess || wide_prepare(c) != cudaSuccess ||
       select_prepare(c) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
+  if ((int64_t)max_sched * c.world > select_cluster_capacity()) return fail(TRAIL_ERR_CAPACITY);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(TRAIL_ERR_CUDA);
   *out = h;
   return TRAIL_OK;
@@ -388,6 +391,43 @@ trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode) {
   return TRAIL_OK;
 }
 
+trail_status trail_set_w1_l2_persist(trail_handle h, int32_t enable) {
+  if (!h || enable < 0 || enable > 1) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  const size_t w1_bytes = (size_t)c.H * c.d * c.esize;
+  if (enable) {
+    int max_persist = 0, max_window = 0;
+    if (cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c.device) !=
+            cudaSuccess ||
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, c.device) !=
+            cudaSuccess)
+      return TRAIL_ERR_CUDA;
+    if (max_persist <= 0 || max_window <= 0) return TRAIL_ERR_UNSUPPORTED;
+    const size_t set_aside = std::min(w1_bytes, (size_t)max_persist);
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, set_aside) != cudaSuccess)
+      return TRAIL_ERR_CUDA;
+    c.w1_window.base_ptr = c.w1;
+    c.w1_window.num_bytes = std::min(w1_bytes, (size_t)max_window);
+    c.w1_window.hitRatio = std::min(1.0f, (float)set_aside / (float)c.w1_window.num_bytes);
+    c.w1_window.hitProp = cudaAccessPropertyPersisting;
+    c.w1_window.missProp = cudaAccessPropertyStreaming;
+    c.w1_persist = true;
+  } else {
+    c.w1_persist = false;
+    if (cudaCtxResetPersistingL2Cache() != cudaSuccess ||
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0) != cudaSuccess)
+      return TRAIL_ERR_CUDA;
+  }
+  return TRAIL_OK;
+}
+
+trail_status trail_set_fill_mode(trail_handle h, int32_t mode) {
+  if (!h || mode < 0 || mode > 1) return TRAIL_ERR_INVALID;
+  h->c.fill_mode = mode;
+  return TRAIL_OK;
+}
+
 trail_status trail_set_threshold_mode(trail_handle h, int32_t mode) {
   if (!h || mode < 0 || mode > 1) return TRAIL_ERR_INVALID;
   Ctx &c = h->c;
@@ -414,6 +454,11 @@ trail_status trail_plan_l1(trail_handle h, int32_t n, int32_t *l1_mode_out, int3
   return TRAIL_OK;
 }
 
+static trail_status predict_body(Ctx &c, const void *emb, int64_t emb_ld,
+                                 const int32_t *row_offsets, const uint32_t *request_ids,
+                                 const uint8_t *is_prefill, const float *prior_override, int32_t n,
+                                 float *posteriors, float *expected_remaining, cudaStream_t s);
+
 trail_status trail_predict_step(trail_handle h, const void *emb, int64_t emb_ld,
                                 const int32_t *row_offsets, const uint32_t *request_ids,
                                 const uint8_t *is_prefill, const float *prior_override,
@@ -428,7 +473,72 @@ trail_status trail_predict_step(trail_handle h, const void *emb, int64_t emb_ld,
   if (emb_ld < c.d || (emb_ld * (int64_t)c.esize) % 16 != 0 || ((uintptr_t)emb) % 16 != 0)
     return TRAIL_ERR_INVALID;
   if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  return predict_body(c, emb, emb_ld, row_offsets, request_ids, is_prefill, prior_override, n,
+                      posteriors, expected_remaining, (cudaStream_t)stream);
+}
+
+trail_status trail_predict_step_layers(trail_handle h, const void *const *embs,
+                                       const float *layer_weights, int32_t n_layers,
+                                       int64_t emb_ld, const int32_t *row_offsets,
+                                       const uint32_t *request_ids, const uint8_t *is_prefill,
+                                       const float *prior_override, int32_t n, float *posteriors,
+                                       float *expected_remaining, trail_stream stream) {
+  if (!h) return TRAIL_ERR_INVALID;
+  Ctx &c = h->c;
+  if (n < 0 || n_layers < 1 || n_layers > kMaxLayers || !embs || !layer_weights)
+    return TRAIL_ERR_INVALID;
+  if (n == 0) return TRAIL_OK;
+  if (n > c.cfg.max_requests) return TRAIL_ERR_CAPACITY;
+  if (!row_offsets || !request_ids || !is_prefill) return TRAIL_ERR_INVALID;
+  if (emb_ld < c.d || (emb_ld * (int64_t)c.esize) % 16 != 0) return TRAIL_ERR_INVALID;
+  double wsum = 0.0;
+  for (int l = 0; l < n_layers; ++l) {
+    if (!embs[l] || ((uintptr_t)embs[l]) % 16 != 0) return TRAIL_ERR_INVALID;
+    if (!(layer_weights[l] >= 0.f) || !std::isfinite(layer_weights[l])) return TRAIL_ERR_INVALID;
+    wsum += (double)layer_weights[l];
+  }
+  if (!(wsum > 0.0)) return TRAIL_ERR_INVALID;
+  if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
+  if (!c.xmix) {   // lazily: [max_requests][d] probe inputs + the one-row-per-request offsets
+    if (cudaMalloc(&c.xmix, (size_t)c.cfg.max_requests * c.d * c.esize) != cudaSuccess ||
+        cudaMalloc(&c.iota, ((size_t)c.cfg.max_requests + 1) * sizeof(int32_t)) != cudaSuccess)
+      return TRAIL_ERR_NOMEM;
+    std::vector<int32_t> io((size_t)c.cfg.max_requests + 1);
+    for (size_t i = 0; i < io.size(); ++i) io[i] = (int32_t)i;
+    if (cudaMemcpy(c.iota, io.data(), io.size() * sizeof(int32_t), cudaMemcpyHostToDevice) !=
+        cudaSuccess)
+      return TRAIL_ERR_CUDA;
+  }
+  MixArgs ma = {};
+  ma.L = n_layers;
+  for (int l = 0; l < n_layers; ++l) {
+    ma.emb[l] = embs[l];
+    ma.a[l] = (double)layer_weights[l] / wsum;
+  }
   cudaStream_t s = (cudaStream_t)stream;
+  {
+    ProfScope p(c, TRAIL_K_POOL, s);
+    TRAIL_CUDA(launch_layer_mix(c, ma, emb_ld, row_offsets, n, s));
+  }
+  return predict_body(c, c.xmix, c.d, c.iota, request_ids, is_prefill, prior_override, n,
+                      posteriors, expected_remaining, s);
+}
+
+namespace trail {
+thread_local const cudaAccessPolicyWindow *tl_l1_window = nullptr;
+}
+
+namespace {
+struct L1Window {        // scope of the layer-1 launches of one predict step
+  explicit L1Window(const Ctx &c) { tl_l1_window = c.w1_persist ? &c.w1_window : nullptr; }
+  ~L1Window() { tl_l1_window = nullptr; }
+};
+}  // namespace
+
+static trail_status predict_body(Ctx &c, const void *emb, int64_t emb_ld,
+                                 const int32_t *row_offsets, const uint32_t *request_ids,
+                                 const uint8_t *is_prefill, const float *prior_override, int32_t n,
+                                 float *posteriors, float *expected_remaining, cudaStream_t s) {
   int mode, bn, splits;
   plan_l1(c, n, &mode, &bn, &splits);
   if (mode != TRAIL_L1_UMMA && mode != TRAIL_L1_WIDE && (size_t)splits * n * c.H > c.partial_elems)
@@ -438,6 +548,7 @@ trail_status trail_predict_step(trail_handle h, const void *emb, int64_t emb_ld,
     // decode rows are gathered from emb by every layer-1 kernel except the unfused GEMM
     TRAIL_CUDA(launch_pool(c, emb, emb_ld, row_offsets, n, mode == TRAIL_L1_UMMA_UNFUSED ? 1 : 0, s));
   }
+  L1Window l1w(c);              // W1 access-policy window (if enabled) on the layer-1 launches
   if (mode == TRAIL_L1_WIDE) {   // layer 1 + layer 2 + head, CTA pairs over the whole hidden width
     ProfScope p(c, TRAIL_K_UMMA, s);
     TRAIL_CUDA(launch_wide_predict(c, emb, emb_ld, row_offsets, n, request_ids, is_prefill,
@@ -458,6 +569,7 @@ trail_status trail_predict_step(trail_handle h, const void *emb, int64_t emb_ld,
     ProfScope p(c, TRAIL_K_UMMA, s);
     TRAIL_CUDA(launch_umma_l1(c, n, bn, splits, s));
   }
+  tl_l1_window = nullptr;        // the head reads no W1
   {
     ProfScope p(c, TRAIL_K_HEAD, s);
     TRAIL_CUDA(launch_head(c, n, splits, request_ids, is_prefill, prior_override, posteriors,
@@ -500,18 +612,18 @@ trail_status trail_time_update(trail_handle h, const uint32_t *request_ids, int3
 
 trail_status trail_schedule_pack(trail_handle h, const uint32_t *request_ids,
                                  const uint32_t *arrival_seq, const int32_t *kv_blocks,
-                                 const uint8_t *is_running, int32_t n, void *records,
-                                 trail_stream stream) {
-  if (!h || n < 0) return TRAIL_ERR_INVALID;
+                                 const uint8_t *is_running, int32_t n, int32_t capacity,
+                                 void *records, trail_stream stream) {
+  if (!h || n < 0 || capacity < n) return TRAIL_ERR_INVALID;
   Ctx &c = h->c;
-  if (n == 0) return TRAIL_OK;
-  if (!request_ids || !arrival_seq || !kv_blocks || !is_running || !records)
+  if (capacity == 0) return TRAIL_OK;
+  if (!records || (n > 0 && (!request_ids || !arrival_seq || !kv_blocks || !is_running)))
     return TRAIL_ERR_INVALID;
   if (set_device(c) != TRAIL_OK) return TRAIL_ERR_CUDA;
   cudaStream_t s = (cudaStream_t)stream;
   ProfScope p(c, TRAIL_K_PACK, s);
   TRAIL_CUDA(launch_pack(c, request_ids, arrival_seq, kv_blocks, is_running, n, (Record *)records,
-                         n, s));
+                         capacity, s));
   return TRAIL_OK;
 }
 
@@ -722,32 +834,16 @@ int select_impl() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("TRAIL_SELECT");
-    v = (e && e[0] == 'b') ? 2 : (e && e[0] == 'r') ? 1 : 0;
+    v = (e && e[0] == 'c') ? 2 : 0;   // "cluster": the single-cluster kernel for every size
   }
   return v;
 }
-bool use_bitonic_select() { return select_impl() == 2; }
-int select_local_capacity() {
-  switch (select_impl()) {
-    case 0: return kRankMaxRecords;
-    case 1: return select_radix_capacity();
-    default: return select_fast_capacity();
-  }
-}
+int select_local_capacity() { return select_cluster_capacity(); }
 cudaError_t launch_select_local(const Ctx &c, const uint32_t *ids, const uint32_t *arrival,
                                 const int32_t *kv, const uint8_t *running, int n, int64_t budget,
                                 int max_run, uint32_t *run, uint32_t *pre, uint32_t *adm,
                                 int32_t *counts, cudaStream_t s) {
-  switch (select_impl()) {
-    case 0:
-      return launch_select_rank(c, nullptr, c.rec_local, ids, arrival, kv, running, n, budget,
-                                max_run, run, pre, adm, counts, s);
-    case 1:
-      return launch_select_radix(c, nullptr, c.rec_local, ids, arrival, kv, running, n, budget,
-                                 max_run, run, pre, adm, counts, s);
-    default:
-      return launch_select_fast(c, nullptr, c.rec_local, ids, arrival, kv, running, n, budget,
-                                max_run, run, pre, adm, counts, s);
-  }
+  return launch_select_any(c, nullptr, c.rec_local, ids, arrival, kv, running, n, budget,
+                           max_run, run, pre, adm, counts, s);
 }
 }  // namespace trail

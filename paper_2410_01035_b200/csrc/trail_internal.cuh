@@ -54,6 +54,42 @@ __host__ __device__ __forceinline__ uint32_t dynamic_threshold(float c, float L)
   return t >= 4294967040.f ? 0xFFFFFFFEu : (t <= 0.f ? 0u : (uint32_t)t);
 }
 
+// Row a4 (record build): key = L_t of the slot (E_pi[L] if never observed, D-24); forced =
+// running & observed & a >= threshold (rank -inf); a bad slot id keys +inf
+// (sorts last, never displaces a valid request) and a negative KV counts 0, both flagged.
+__device__ __forceinline__ Record build_record(uint32_t slot, uint32_t arrival, int32_t kvb,
+                                               bool run, const SlotMeta *__restrict__ meta,
+                                               const HeadConsts *__restrict__ cst,
+                                               int max_slots, uint32_t id_base,
+                                               uint32_t *__restrict__ err) {
+  if (kvb < 0) { atomicOr(err, TRAIL_DEV_NEG_KV); kvb = 0; }
+  float key = cst->prior_L;
+  bool forced = false;
+  if (slot < (uint32_t)max_slots) {
+    const SlotMeta mt = meta[slot];
+    if (mt.flags & 1u) {
+      key = mt.L;
+      forced = run && (mt.age >= mt.thr);
+    }
+  } else {
+    atomicOr(err, TRAIL_DEV_BAD_ID);
+    key = INFINITY;
+  }
+  uint32_t kb;
+  if (isfinite(key) && key >= 0.f) {
+    kb = __float_as_uint(key) & 0x7FFFFFFFu;
+  } else {
+    if (slot < (uint32_t)max_slots) atomicOr(err, TRAIL_DEV_NONFIN);
+    kb = 0x7F800000u;
+  }
+  Record r;
+  r.keybits = (forced ? 0u : 0x80000000u) | kb;
+  r.arrival = arrival;
+  r.kv = (uint32_t)kvb;
+  r.gid = ((id_base + slot) & 0x7FFFFFFFu) | (run ? 0x80000000u : 0u);
+  return r;
+}
+
 struct Ctx {
   trail_config cfg;
   int device = 0;
@@ -79,6 +115,8 @@ struct Ctx {
   int fused_max_clusters[17] = {};
   float *chunk_acc = nullptr;       // [max_slots][d] chunked-prefill running sums (lazy)
   uint32_t *chunk_cnt = nullptr;    // [max_slots] rows accumulated so far
+  void *xmix = nullptr;             // [max_requests][d] multi-layer probe inputs (lazy)
+  int32_t *iota = nullptr;          // [max_requests + 1] 0, 1, 2, ... (one row per request)
   float *pool_head = nullptr;       // [pool_grid][d] K1 partial sums (request began earlier)
   float *pool_tail = nullptr;       // [pool_grid][d] K1 partial sums (request continues)
   uint32_t *pool_cnt = nullptr;     // [max_requests] K1 per-request chunk arrival counters
@@ -88,8 +126,6 @@ struct Ctx {
   uint32_t *rank_cnt = nullptr;     // rank-select CTA completion counter  // fused kernel: resident clusters of size s (occupancy)
   Record *rec_local = nullptr; // [max_sched]
   Record *rec_all = nullptr;   // [max_sched * world]
-  void *sel_scratch = nullptr; // global scratch for large selections
-  size_t sel_scratch_bytes = 0;
   // TMA descriptors (bf16 path)
   CUtensorMap tmap_x, tmap_w128, tmap_w256;
   CUtensorMap tmap_w_gemv;                       // W1, 16-byte x 64-row boxes (K2a)
@@ -102,6 +138,9 @@ struct Ctx {
   bool have_tmaps = false;
   int num_sms = 148;
   int64_t rows_hint = 0;        // trail_set_rows_hint: embedding rows of the next predict steps
+  int fill_mode = 0;            // trail_set_fill_mode: 0 strict prefix (D-15), 1 first-fit
+  bool w1_persist = false;      // trail_set_w1_l2_persist
+  cudaAccessPolicyWindow w1_window = {};
   // NCCL
   void *nccl_comm = nullptr;
   int rank = 0, world = 1;
@@ -145,6 +184,14 @@ cudaError_t launch_select(const Ctx &c, const Record *rec, int n, int64_t budget
                           cudaStream_t s);
 cudaError_t launch_time_update(const Ctx &c, const uint32_t *ids, int n, int steps, float *post,
                                float *L, cudaStream_t s);
+constexpr int kMaxLayers = 8;
+struct MixArgs {                  // multi-layer weighted embeddings (k_mix.cu, reading D-28)
+  const void *emb[kMaxLayers];
+  double a[kMaxLayers];           // normalised weights (fp64, host)
+  int L;
+};
+cudaError_t launch_layer_mix(Ctx &c, const MixArgs &ma, int64_t ld, const int32_t *off, int n,
+                             cudaStream_t s);
 cudaError_t launch_prefill_chunk(Ctx &c, const void *emb, int64_t ld, const int32_t *off,
                                  const uint32_t *ids, const uint8_t *is_final, int n,
                                  void *pooled, int64_t pld, cudaStream_t s);
@@ -170,16 +217,26 @@ cudaError_t launch_wide_predict(Ctx &c, const void *emb, int64_t ld, const int32
                                 const float *prior_override, float *post, float *L,
                                 cudaStream_t s);
 cudaError_t select_prepare(Ctx &c);
-cudaError_t select_radix_prepare();
-int select_radix_capacity();
-cudaError_t launch_select_radix(const Ctx &c, const Record *rec_in, Record *rec_out,
-                                const uint32_t *ids, const uint32_t *arrival, const int32_t *kv,
-                                const uint8_t *running, int n, int64_t budget, int max_run,
-                                uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
-                                cudaStream_t s);
-bool use_bitonic_select();
+// K4 selection: one thread-block cluster (k_csort.cu).  rec_in != nullptr: select over given
+// records; else build the local records (fused K5 pack) from (ids, arrival, kv, running)
+// into rec_out and select over them.
+cudaError_t select_cluster_prepare();
+int select_cluster_capacity();
+cudaError_t launch_select_cluster(const Ctx &c, const Record *rec_in, Record *rec_out,
+                                  const uint32_t *ids, const uint32_t *arrival, const int32_t *kv,
+                                  const uint8_t *running, int m, int64_t budget, int max_run,
+                                  uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
+                                  cudaStream_t s);
+// default dispatch: rank-counting kernel (k_rank.cu) up to kRankMaxRecords records, the
+// bucketed kernels (k_bucket.cu) above; the cluster kernel for first-fit filling and as
+// TRAIL_SELECT=cluster
 int select_impl();
 int select_local_capacity();
+cudaError_t launch_select_any(const Ctx &c, const Record *rec_in, Record *rec_out,
+                              const uint32_t *ids, const uint32_t *arrival, const int32_t *kv,
+                              const uint8_t *running, int n, int64_t budget, int max_run,
+                              uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
+                              cudaStream_t s);
 cudaError_t launch_select_local(const Ctx &c, const uint32_t *ids, const uint32_t *arrival,
                                 const int32_t *kv, const uint8_t *running, int n, int64_t budget,
                                 int max_run, uint32_t *run, uint32_t *pre, uint32_t *adm,
@@ -187,28 +244,18 @@ cudaError_t launch_select_local(const Ctx &c, const uint32_t *ids, const uint32_
 cudaError_t select_rank_prepare();
 cudaError_t select_bucket_prepare();
 size_t bucket_workspace_bytes(int m_max);
-cudaError_t launch_select_bucket(const Ctx &c, const Record *rec, int m, int64_t budget,
+cudaError_t launch_select_bucket(const Ctx &c, const Record *rec_in, Record *rec_out,
+                                 const uint32_t *ids, const uint32_t *arrival, const int32_t *kv,
+                                 const uint8_t *running, int m, int64_t budget,
                                  int max_run, uint32_t *run, uint32_t *pre, uint32_t *adm,
                                  int32_t *counts, cudaStream_t s);
-constexpr int kRankMaxRecords = 2048;   // rank-counting kernel below, bucketed kernels above
-int select_rank_capacity();
+constexpr int kRankMaxRecords = 2048;
 cudaError_t launch_select_rank(const Ctx &c, const Record *rec_in, Record *rec_out,
                                const uint32_t *ids, const uint32_t *arrival, const int32_t *kv,
                                const uint8_t *running, int n, int64_t budget, int max_run,
                                uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
                                cudaStream_t s);
-cudaError_t select_fast_prepare();
-int select_fast_capacity();
-// rec_in != nullptr: select over given records; else build local records (fused pack)
-// from (ids, arrival, kv, running) into rec_out and select over them.
-cudaError_t launch_select_fast(const Ctx &c, const Record *rec_in, Record *rec_out,
-                               const uint32_t *ids, const uint32_t *arrival, const int32_t *kv,
-                               const uint8_t *running, int n, int64_t budget, int max_run,
-                               uint32_t *run, uint32_t *pre, uint32_t *adm, int32_t *counts,
-                               cudaStream_t s);
 cudaError_t head_prepare(Ctx &c);
-size_t select_scratch_bytes(int n_max);
-int select_smem_capacity();
 
 // ---------------------------------------------------------------- launch helper
 // Programmatic dependent launch (PDL): consecutive kernels of a step overlap the next
@@ -218,6 +265,20 @@ int select_smem_capacity();
 // starve it of SM resources).
 bool pdl_enabled();
 
+// L2-persisting W1 (optional; trail_set_w1_l2_persist): while a layer-1 kernel
+// is launched, this points at the access-policy window over W1 and every launch made through
+// launch_k / add_l1_window carries it (set and cleared by predict_body, one host thread per
+// handle).
+extern thread_local const cudaAccessPolicyWindow *tl_l1_window;
+inline int add_l1_window(cudaLaunchAttribute *attr, int na) {
+  if (tl_l1_window) {
+    attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[na].val.accessPolicyWindow = *tl_l1_window;
+    ++na;
+  }
+  return na;
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args... args) {
@@ -226,11 +287,16 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  na = add_l1_window(attr, na);
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 

@@ -37,7 +37,8 @@ def init_comm(trail, group=None) -> None:
 
 
 def pad_records(records, n: int):
-    """Mark records [n, cap) as padding (in place).  `records` is an int32 [cap, 4] tensor."""
+    """Mark records [n, cap) as padding (in place) — for records built outside the library
+    (the CPU tests); trail_schedule_pack pads its own output.  int32 [cap, 4] tensor."""
     if n < records.shape[0]:
         records[n:].fill_(PAD_WORD)
     return records
@@ -62,9 +63,8 @@ def schedule_torch_collective(trail, request_ids, arrival_seq, kv_blocks, is_run
     n = int(request_ids.shape[0])
     cap = int(cap or trail.max_sched)
     local = torch.empty((cap, RECORD_BYTES // 4), dtype=torch.int32, device=request_ids.device)
-    trail_schedule_pack(trail.h, request_ids, arrival_seq, kv_blocks, is_running, n, local,
-                        stream)
-    pad_records(local, n)
+    trail_schedule_pack(trail.h, request_ids, arrival_seq, kv_blocks, is_running, n, cap, local,
+                        stream)   # records [n, cap) are written as padding by the kernel
     allrec = gather_records(local, group)
     trail_schedule_select(trail.h, allrec, allrec.shape[0], kv_budget, max_run, trail.run_ids,
                           trail.preempt_ids, trail.admit_ids, trail.counts, stream)

@@ -67,8 +67,10 @@ _SIGS = {
     "trail_create": ([ctypes.POINTER(trail_config), ctypes.POINTER(_P)], _I32),
     "trail_destroy": ([_P], _I32),
     "trail_predict_step": ([_P, _P, _I64, _P, _P, _P, _P, _I32, _P, _P, _P], _I32),
+    "trail_predict_step_layers": ([_P, _P, _P, _I32, _I64, _P, _P, _P, _P, _I32, _P, _P, _P],
+                                  _I32),
     "trail_schedule_step": ([_P, _P, _P, _P, _P, _I32, _I64, _I32, _P, _P, _P, _P, _P], _I32),
-    "trail_schedule_pack": ([_P, _P, _P, _P, _P, _I32, _P, _P], _I32),
+    "trail_schedule_pack": ([_P, _P, _P, _P, _P, _I32, _I32, _P, _P], _I32),
     "trail_schedule_select": ([_P, _P, _I32, _I64, _I32, _P, _P, _P, _P, _P], _I32),
     "trail_release": ([_P, _P, _I32, _P], _I32),
     "trail_read_state": ([_P, _P, _I32, _P, _P, _P, _P, _P, _P], _I32),
@@ -83,6 +85,8 @@ _SIGS = {
     "trail_time_update": ([_P, _P, _I32, _I32, _P, _P, _P], _I32),
     "trail_prefill_chunk": ([_P, _P, _I64, _P, _P, _P, _I32, _P, _I64, _P], _I32),
     "trail_set_threshold_mode": ([_P, _I32], _I32),
+    "trail_set_fill_mode": ([_P, _I32], _I32),
+    "trail_set_w1_l2_persist": ([_P, _I32], _I32),
     "trail_trace_enable": ([_P, _I32], _I32),
     "trail_trace_read": ([_P, _P, _I32], _I32),
     "trail_plan_l1": ([_P, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)], _I32),
@@ -163,6 +167,30 @@ def trail_predict_step(h, emb, emb_ld, row_offsets, request_ids, is_prefill, pri
         _stream(stream)))
 
 
+def trail_predict_step_layers(h, embs, layer_weights, emb_ld, row_offsets, request_ids,
+                              is_prefill, prior_override, n, posteriors, expected_remaining,
+                              stream=None) -> int:
+    """Multi-layer weighted embeddings (D-28): `embs` a list of device tensors / pointers,
+    `layer_weights` host floats; marshalled into the (host) pointer and weight arrays."""
+    L = len(embs)
+    ptrs = (ctypes.c_void_p * L)(*[_ptr(e) for e in embs])
+    ws = (ctypes.c_float * L)(*[float(x) for x in layer_weights])
+    return _check("trail_predict_step_layers", _lib().trail_predict_step_layers(
+        h, ctypes.cast(ptrs, ctypes.c_void_p), ctypes.cast(ws, ctypes.c_void_p), L, int(emb_ld),
+        _ptr(row_offsets), _ptr(request_ids), _ptr(is_prefill), _ptr(prior_override), int(n),
+        _ptr(posteriors), _ptr(expected_remaining), _stream(stream)))
+
+
+def trail_set_w1_l2_persist(h, enable: int) -> int:
+    """L2-persisting W1 for the layer-1 kernels (device-wide set-aside)."""
+    return _check("trail_set_w1_l2_persist", _lib().trail_set_w1_l2_persist(h, int(enable)))
+
+
+def trail_set_fill_mode(h, mode: int) -> int:
+    """0 = strict prefix (D-15), 1 = first-fit."""
+    return _check("trail_set_fill_mode", _lib().trail_set_fill_mode(h, int(mode)))
+
+
 def trail_schedule_step(h, request_ids, arrival_seq, kv_blocks, is_running, n, kv_budget,
                         max_run, run_ids, preempt_ids, admit_ids, counts, stream=None) -> int:
     return _check("trail_schedule_step", _lib().trail_schedule_step(
@@ -171,11 +199,11 @@ def trail_schedule_step(h, request_ids, arrival_seq, kv_blocks, is_running, n, k
         _ptr(counts), _stream(stream)))
 
 
-def trail_schedule_pack(h, request_ids, arrival_seq, kv_blocks, is_running, n, records,
-                        stream=None) -> int:
+def trail_schedule_pack(h, request_ids, arrival_seq, kv_blocks, is_running, n, capacity,
+                        records, stream=None) -> int:
     return _check("trail_schedule_pack", _lib().trail_schedule_pack(
         h, _ptr(request_ids), _ptr(arrival_seq), _ptr(kv_blocks), _ptr(is_running), int(n),
-        _ptr(records), _stream(stream)))
+        int(capacity), _ptr(records), _stream(stream)))
 
 
 def trail_schedule_select(h, records, n_records, kv_budget, max_run, run_ids, preempt_ids,
@@ -333,6 +361,15 @@ class Trail:
             self._rows_hint = rows
         trail_predict_step(self.h, emb, emb.shape[1] if emb.dim() == 2 else self.d, row_offsets,
                            request_ids, is_prefill, prior_override, n, self.post, self.L, stream)
+        return self.post[:n], self.L[:n]
+
+    def predict_layers(self, embs, layer_weights, row_offsets, request_ids, is_prefill,
+                       prior_override=None, stream=None):
+        """Probe on the weighted average of several layers' embeddings."""
+        n = int(request_ids.shape[0])
+        ld = embs[0].shape[1] if embs[0].dim() == 2 else self.d
+        trail_predict_step_layers(self.h, embs, layer_weights, ld, row_offsets, request_ids,
+                                  is_prefill, prior_override, n, self.post, self.L, stream)
         return self.post[:n], self.L[:n]
 
     def time_update(self, request_ids, steps: int, stream=None):

@@ -10,14 +10,26 @@ the embedding carries the score vector s in its first k coordinates and the prob
 W1 = [I; -I; 0], b1 = 0, W2 = [I, -I, 0], b2 = 0, so z = ReLU(s) - ReLU(-s) = s and the GPU's
 softmax is the model's p (up to bf16 rounding of s).
 
-Reports mean latency, mean TTFT (iterations) and preemptions per policy c.  Diagnostic /
+Policies: TRAIL with preemption parameter c, and the vLLM-FCFS baseline the paper
+compares against: the same library selection fed NO predictions — every key is
+then E_pi[L] and ties go to the earlier arrival (D-18, D-24), so the run set is the longest
+arrival-ordered prefix within the KV budget and the latest arrivals are the ones preempted,
+which is vLLM's FCFS admission + recompute preemption.  Arrivals: Poisson per iteration
+ or one burst of every job at iteration 0.  Memory: "hold" (a preempted job
+keeps its context; only the run set's KV counts) or discard-and-recompute (a
+preempted job rebuilds its context at `recompute_rate` tokens per iteration when it runs
+again, emitting nothing meanwhile).
+
+Reports mean latency, mean TTFT (iterations) and preemptions per policy.  Diagnostic /
 demonstration tool — the product path is only the library calls it makes.
 
   python scripts/simulate.py [--jobs 2000] [--rate 6] [--budget-frac 0.35] [--c 0,0.5,0.8,inf]
+                             [--fcfs] [--arrivals poisson|burst] [--grid] [--out FILE]
 """
 from __future__ import annotations
 
 import argparse
+import json
 import math
 import os
 import sys
@@ -42,15 +54,21 @@ def probe_weights(d: int, H: int, k: int, edges: np.ndarray) -> dict:
             "b2": np.zeros(k, np.float32), "edges": edges}
 
 
-def run(c: float, args, seed: int) -> dict:
+def run(c: float, args, seed: int, fcfs: bool = False) -> dict:
+    """One simulation; c is ignored for the FCFS baseline (no predictions are made)."""
     rs = np.random.default_rng(seed)
     k, d, H = 10, 256, 128
     edges = W.paper_bin_edges(k)
     m = (edges[:-1] + edges[1:]) / 2
     w = edges[1] - edges[0]
     n_jobs = args.jobs
-    # workload: Poisson arrivals per iteration, Alpaca-like output lengths
-    arr = np.cumsum(rs.exponential(1.0 / args.rate, n_jobs)).astype(np.int64)
+    # workload: Poisson arrivals per iteration (P:437) or one burst at t = 0 (P:570),
+    # Alpaca-like output lengths (P:201)
+    if getattr(args, "arrivals", "poisson") == "burst":
+        arr = np.zeros(n_jobs, np.int64)
+        rs.exponential(1.0, n_jobs)                     # keep the size draws aligned
+    else:
+        arr = np.cumsum(rs.exponential(1.0 / args.rate, n_jobs)).astype(np.int64)
     size = np.clip(np.round(rs.lognormal(math.log(150), 0.9, n_jobs)), 1, 512).astype(np.int64)
     plen = np.clip(np.round(rs.lognormal(math.log(32), 0.7, n_jobs)), 4, 512).astype(np.int64)
     slots = args.slots
@@ -119,9 +137,11 @@ def run(c: float, args, seed: int) -> dict:
         emb = np.zeros((len(batch), d), np.float32)
         emb[:, :k] = score
         pref = np.array([j not in observed for j in batch], np.uint8)
-        t.predict(dv(W.encode(emb, "bf16").view(np.int16)), dv(np.arange(len(batch) + 1, dtype=np.int32)),
-                  dv(np.array([live[j] for j in batch], np.int32)), dv(pref))
-        observed.update(batch)
+        if not fcfs:   # the FCFS baseline makes no predictions
+            t.predict(dv(W.encode(emb, "bf16").view(np.int16)),
+                      dv(np.arange(len(batch) + 1, dtype=np.int32)),
+                      dv(np.array([live[j] for j in batch], np.int32)), dv(pref))
+            observed.update(batch)
         fin = [j for j in batch if gen[j] >= size[j]]
         if fin:
             t.release(dv(np.array([live[j] for j in fin], np.int32)))
@@ -137,8 +157,24 @@ def run(c: float, args, seed: int) -> dict:
     lat = (done - arr)[ok]
     ttft = (first - arr)[ok] + 1
     warm = int(0.2 * ok.sum())
-    return {"c": c, "completed": int(ok.sum()), "iters": it, "mean_latency": float(lat[warm:].mean()),
-            "mean_ttft": float(ttft[warm:].mean()), "preemptions": preempt}
+    if getattr(args, "arrivals", "poisson") == "burst":
+        warm = 0                          # a burst has no steady state: every job counts
+    return {"policy": "fcfs" if fcfs else "trail", "c": "inf" if math.isinf(c) else c,
+            "completed": int(ok.sum()), "iters": it,
+            "mean_latency": float(lat[warm:].mean()) if ok.any() else None,
+            "mean_ttft": float(ttft[warm:].mean()) if ok.any() else None,
+            "preemptions": preempt}
+
+
+def summarize(c, args, fcfs=False):
+    rows = [run(c, args, 1000 + s, fcfs=fcfs) for s in range(args.seeds)]
+    return {"policy": "fcfs" if fcfs else "trail", "c": rows[0]["c"],
+            "arrivals": args.arrivals, "budget_frac": args.budget_frac,
+            "recompute_rate": args.recompute_rate, "rate": args.rate,
+            "mean_latency": float(np.mean([r["mean_latency"] for r in rows])),
+            "mean_ttft": float(np.mean([r["mean_ttft"] for r in rows])),
+            "preemptions": float(np.mean([r["preemptions"] for r in rows])),
+            "completed": rows[0]["completed"], "iters": rows[0]["iters"], "seeds": args.seeds}
 
 
 def main():
@@ -154,14 +190,27 @@ def main():
                     help="discard mode: tokens of context rebuilt per iteration (0 = hold mode)")
     ap.add_argument("--seeds", type=int, default=2)
     ap.add_argument("--max-iters", type=int, default=200000)
+    ap.add_argument("--arrivals", default="poisson", choices=["poisson", "burst"])
+    ap.add_argument("--fcfs", action="store_true", help="also run the vLLM-FCFS baseline")
+    ap.add_argument("--grid", action="store_true",
+                    help="memory sensitivity grid: budget x recompute rate x arrivals")
+    ap.add_argument("--out", default=None, help="write all rows as JSON")
     args = ap.parse_args()
-    for cs in args.c.split(","):
-        c = math.inf if cs == "inf" else float(cs)
-        rows = [run(c, args, 1000 + s) for s in range(args.seeds)]
-        print({"c": c, "mean_latency": float(np.mean([r["mean_latency"] for r in rows])),
-               "mean_ttft": float(np.mean([r["mean_ttft"] for r in rows])),
-               "preemptions": float(np.mean([r["preemptions"] for r in rows])),
-               "completed": rows[0]["completed"], "iters": rows[0]["iters"]}, flush=True)
+    cs = [math.inf if v == "inf" else float(v) for v in args.c.split(",")]
+    grid = ([(bf, rr, ar) for ar in ("poisson", "burst") for bf in (0.15, 0.25, 0.35)
+             for rr in (0.0, 4.0, 16.0)] if args.grid
+            else [(args.budget_frac, args.recompute_rate, args.arrivals)])
+    out = []
+    for bf, rr, ar in grid:
+        args.budget_frac, args.recompute_rate, args.arrivals = bf, rr, ar
+        rows = ([summarize(0.0, args, fcfs=True)] if (args.fcfs or args.grid) else [])
+        rows += [summarize(c, args) for c in cs]
+        for r in rows:
+            print(json.dumps(r), flush=True)
+        out += rows
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump({"args": vars(args), "rows": out}, f, indent=1)
 
 
 if __name__ == "__main__":

@@ -423,3 +423,37 @@ def test_prefill_chunk_oracle_is_the_mean_of_all_rows():
     o.release(np.array([5]))
     nxt = o.prefill_chunk(full[20:], np.array([0, 17]), np.array([5]), np.array([1]))
     np.testing.assert_allclose(nxt[0], full[20:].mean(axis=0), rtol=1e-12, atol=1e-15)
+
+
+# ----------------------------------------------------------------------------- multi-layer
+def test_multi_layer_weighted_average_oracle():
+    """Multi-layer weighted embeddings (reading D-28): u = sum_l a_l u_l with
+    a = w / sum(w).  Pins: one layer (or identical layers, any weights) is the plain
+    predict_step; weights [3, 1] on a hand-computed 2-d example give 0.75 u_1 + 0.25 u_2 of
+    the per-layer prompt means; a zero weight drops its layer."""
+    w_ = W.make_weights(64, 128, 10, "f32", seed=8)
+    mk = lambda: R.TrailOracle(w_["W1"], w_["b1"], w_["W2"], w_["b2"], w_["edges"], 0.8, 8,  # noqa: E731
+                               x_dtype="f32")
+    rs = np.random.default_rng(4)
+    e1, e2 = rs.standard_normal((9, 64)), rs.standard_normal((9, 64))
+    off, ids, pf = np.array([0, 5, 6, 9]), np.array([0, 1, 2]), np.array([1, 0, 1])
+    q1, L1 = mk().predict_step(e1, off, ids, pf)
+    q2, L2 = mk().predict_step_layers([e1], off, ids, pf, [2.5])
+    np.testing.assert_array_equal(q1, q2)
+    q3, _ = mk().predict_step_layers([e1, e1, e1], off, ids, pf, [1.0, 7.0, 0.5])
+    np.testing.assert_allclose(q3, q1, rtol=1e-12, atol=1e-15)
+    q4, _ = mk().predict_step_layers([e1, e2], off, ids, pf, [1.0, 0.0])
+    np.testing.assert_allclose(q4, q1, rtol=1e-12, atol=1e-15)
+    # hand-computed 2-d example: request rows layer1 [[1,2],[3,6]], layer2 [[5,-2],[7,2]]
+    o = R.TrailOracle(np.eye(2), np.zeros(2), np.zeros((3, 2)), np.zeros(3),
+                      np.array([0.0, 2.0, 4.0, 6.0]), 0.8, 2, x_dtype="f32")
+    X = o.mixed_inputs([np.array([[1.0, 2.0], [3.0, 6.0]]), np.array([[5.0, -2.0], [7.0, 2.0]])],
+                       np.array([0, 2]), [3.0, 1.0])
+    # layer means [2, 4] and [6, 0] -> 0.75 [2, 4] + 0.25 [6, 0] = [3, 3]
+    np.testing.assert_array_equal(X, [[3.0, 3.0]])
+    ob = R.TrailOracle(np.eye(2), np.zeros(2), np.zeros((3, 2)), np.zeros(3),
+                       np.array([0.0, 2.0, 4.0, 6.0]), 0.8, 2, x_dtype="bf16")
+    Xb = ob.mixed_inputs([np.array([[1.0, 1.0]]), np.array([[1.0 + 2.0 ** -7, 1.0]])], np.array([0, 1]),
+                         [1.0, 1.0])
+    # (1 + (1 + 2^-7)) / 2 = 1 + 2^-8: a bf16 tie, rounded once to even -> 1.0
+    np.testing.assert_array_equal(Xb, [[1.0, 1.0]])

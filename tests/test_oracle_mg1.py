@@ -129,3 +129,22 @@ def test_limited_preemption_memory_tradeoff():
             ps.append(mg1.simulate(a, s, r, C)["peak_memory"])
         peaks[C] = np.mean(ps)
     assert peaks[0.5] < peaks[1.0]
+
+
+def test_theory_sweep_small_grid():
+    """§8(f)4 sweep harness (tests/theory_sweep.py) on a small grid: every point has a DES
+    mean within 3 SE + 2 % of the corrected Lemma 1 where the lemma applies, mean response
+    grows with lambda, and peak memory never rises when C shrinks from 2 to 0.25 (App. D:
+    limiting preemption bounds the memory held by preempted jobs)."""
+    import theory_sweep as TS
+    rows = TS.sweep(lams=(0.5, 0.8), cs=("0", 0.25, 1.0, 2.0), predictors=("perfect",),
+                    jobs=60_000, seeds=2)
+    by = {(r["lambda"], r["C"]): r for r in rows}
+    for r in rows:
+        if r["lemma1_corrected"] is not None:
+            tol = 3 * (r["des_se"] or 0.0) + 0.02 * r["lemma1_corrected"]
+            assert abs(r["des_mean_response"] - r["lemma1_corrected"]) <= tol, r
+    for C in ("0", 0.25, 1.0, 2.0):
+        assert by[(0.8, C)]["des_mean_response"] > by[(0.5, C)]["des_mean_response"]
+    for lam in (0.5, 0.8):
+        assert by[(lam, 0.25)]["des_peak_memory"] <= by[(lam, 2.0)]["des_peak_memory"] * 1.0001

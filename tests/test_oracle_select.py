@@ -110,3 +110,59 @@ def test_c_inf_is_pure_sprpt_prefix():
 def test_unlimited_budget_runs_everything():
     for b, (run, pre, adm, st), key, forced, seen in _trajectory(0.8, 1e9):
         assert len(run) == b.m and len(pre) == 0
+
+
+def brute_force_first_fit(key, forced, arrival, kv, budget, max_run):
+    """First-fit by definition, enumerated: among all subsets S with forced c S, sum kv <=
+    budget and |S| <= max_run, the one whose membership vector, read in priority order
+    (forced first, then (key, arrival)), is lexicographically largest — a member ranked
+    earlier always outweighs any set of later ones."""
+    m = len(key)
+    cap = max_run if max_run > 0 else m
+    F = [j for j in range(m) if forced[j]]
+    if sum(kv[j] for j in F) > budget or len(F) > cap:
+        return set(F), R.STATUS_WARN_OVER_BUDGET
+    free = sorted((j for j in range(m) if not forced[j]), key=lambda j: (key[j], arrival[j], j))
+    best, best_vec = None, None
+    for r in range(len(free) + 1):
+        for S in itertools.combinations(free, r):
+            if sum(kv[j] for j in S) + sum(kv[j] for j in F) > budget or len(S) + len(F) > cap:
+                continue
+            vec = tuple(1 if j in S else 0 for j in free)
+            if best_vec is None or vec > best_vec:
+                best, best_vec = set(S), vec
+    return set(F) | best, R.STATUS_OK
+
+
+@pytest.mark.parametrize("trial", range(300))
+def test_first_fit_equals_brute_force(trial):
+    """fill='first_fit' (the D-15 alternative) against its definition."""
+    rs = np.random.default_rng(5000 + trial)
+    m = int(rs.integers(1, 10))
+    key = rs.choice([25.6, 76.8, 128.0, 179.2, 256.0], size=m) + rs.choice([0.0, 0.5], size=m)
+    forced = rs.random(m) < 0.3
+    running = forced | (rs.random(m) < 0.5)
+    arrival = rs.permutation(m) + 10
+    kv = rs.integers(0, 8, size=m)
+    budget = int(rs.integers(0, 30))
+    max_run = int(rs.choice([0, 0, 2, 4]))
+    ids = np.arange(m) + 100
+    run, pre, adm, st = R.select(key, forced, arrival, kv, running, ids, budget, max_run,
+                                 fill="first_fit")
+    exp_set, exp_st = brute_force_first_fit(key, forced, arrival, kv, budget, max_run)
+    assert set(run - 100) == exp_set and st == exp_st
+    assert set(pre - 100) == {j for j in range(m) if running[j] and j not in exp_set}
+    assert set(adm - 100) == {j for j in range(m) if not running[j] and j in exp_set}
+    order = [(0 if forced[j] else 1, key[j], arrival[j]) for j in run - 100]
+    assert order == sorted(order)
+    # first-fit contains the strict prefix
+    run_p = R.select(key, forced, arrival, kv, running, ids, budget, max_run)[0]
+    assert set(run_p) <= set(run)
+
+
+def test_first_fit_example_D15():
+    """Keys A=10, B=20, C=30 with kv 5, 8, 2 and budget 9: first-fit gives {A, C} (SURVEY
+    §8(c) D-15 example)."""
+    run, pre, adm, st = R.select([10.0, 20.0, 30.0], [False] * 3, [0, 1, 2], [5, 8, 2],
+                                 [0, 0, 0], np.array([0, 1, 2]), 9, fill="first_fit")
+    assert list(run) == [0, 2] and list(adm) == [0, 2] and st == R.STATUS_OK
