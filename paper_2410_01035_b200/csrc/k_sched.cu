@@ -17,6 +17,8 @@
 
 namespace trail {
 
+thread_local const cudaAccessPolicyWindow *tl_l1_window = nullptr;   // see trail_internal.cuh
+
 // ------------------------------------------------------------------ K5 pack
 __global__ void trail_pack_kernel(const uint32_t *__restrict__ ids,
                                   const uint32_t *__restrict__ arrival,

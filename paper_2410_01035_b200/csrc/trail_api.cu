@@ -524,10 +524,6 @@ trail_status trail_predict_step_layers(trail_handle h, const void *const *embs,
                       posteriors, expected_remaining, s);
 }
 
-namespace trail {
-thread_local const cudaAccessPolicyWindow *tl_l1_window = nullptr;
-}
-
 namespace {
 struct L1Window {        // scope of the layer-1 launches of one predict step
   explicit L1Window(const Ctx &c) { tl_l1_window = c.w1_persist ? &c.w1_window : nullptr; }
