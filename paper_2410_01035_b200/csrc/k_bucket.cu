@@ -1,25 +1,28 @@
 // K4 (row a6) for large record counts (multi-rank all-gathers, configs 3-5): a bucketed
-// exact ranking in three PDL-chained kernels over the 16-byte records (row a4/a5).
+// exact ranking in four PDL-chained kernels over the 16-byte records (row a4/a5).
 //
-// Same contract as every selection kernel: order = (keybits << 32 | arrival) ascending, ties
-// by gid — forced first (rank -inf), then shortest predicted remaining length
-// (P:171), FCFS ties — run set = all forced + the longest prefix of the rest
-// within the KV budget and run cap (strict prefix D-15, overflow D-16).
+// Same contract as every selection kernel: order = (keybits << 32 | arrival, input position)
+// ascending — forced first (rank -inf), then shortest predicted remaining length
+// (P:171), FCFS ties, then input position (D-18) — run set = all forced + the
+// longest prefix of the rest within the KV budget and run cap (strict prefix D-15, overflow
+// D-16).
 //
 // The key of a record is L_t, a convex combination of the bin midpoints, so it lies in
-// [m_0, m_{k-1}] (create-time constants): buckets are 2 x 1024 equal-width L intervals
-// (forced, then non-forced), a monotone map of the key, so the order is
-//   position(i) = #records in lower buckets + #records of its bucket ordered before it.
+// [m_0, m_{k-1}] (create-time constants): buckets are equal-width L intervals (1024 for the
+// forced class, 1024 for the rest), a monotone map of the key.  One exact tie is systematic:
+// every never-observed request is keyed E_pi[L] (D-24), and a burst of arrivals puts thousands
+// of them on one key; their order is FCFS (arrival), so that key gets its own range of 1024
+// arrival sub-buckets between the lower and the upper part of its L interval.
+//   B0  (local path) the records (row a4, fused pack); arrival range of the E_pi[L] tie group
 //   B1  histogram of (count, KV, running) per bucket (warp-aggregated global atomics)
 //   B2  scatter of the records into bucket order (prefix of the counts, atomic cursors)
 //   B3  each record counts the records of its own bucket ordered before it (the bucket range
-//       is staged in shared memory; 16 threads per record, so a tie cluster of b records is
-//       spread over b/64 CTAs with b/16 compares per thread), adds the bucket prefixes
+//       is staged in shared memory; 16 threads per record), adds the bucket prefixes
 //       -> position, cumulative KV, running-before, and the lists follow as in k_rank.cu
 //       (one packed acq_rel atomic; the last CTA writes the preempt list and re-arms).
-// Cost is O(m + sum over buckets of size^2 / 16); a tie cluster (e.g. never-observed requests,
-// all keyed E_pi[L]) is spread over the CTAs that own its positions.  Equal (key, arrival)
-// pairs are ordered by input position, as in the oracle's stable sort (D-18).
+// Cost is O(m + sum over buckets of size^2 / 16).
+#include <string.h>
+
 #include <algorithm>
 
 #include "trail_internal.cuh"
@@ -27,10 +30,13 @@
 namespace trail {
 
 namespace {
-constexpr int kBH = 1024;               // buckets per class (forced / not forced)
-constexpr int kB = 2 * kBH;
+constexpr int kBH = 1024;               // L buckets per class (forced / not forced)
+constexpr int kTie = 1024;              // arrival sub-buckets of the E_pi[L] tie group
+constexpr int kBUsed = 2 * kBH + 1 + kTie;
+constexpr int kB = 4096;                // bucket slots (kBUsed rounded up; 4 per scan thread)
+static_assert(kBUsed <= kB, "bucket layout exceeds the scanned slots");
 constexpr int kB3Threads = 1024;
-constexpr int kB3Tpi = 16;             // threads per record in B3
+constexpr int kB3Tpi = 16;              // threads per record in B3
 constexpr int kB3Items = kB3Threads / kB3Tpi;
 constexpr int kStageCap = 8192;         // bucket entries staged in shared memory (128 KB)
 
@@ -40,13 +46,33 @@ struct BkEntry {                        // bucket-sorted record (16 B)
   uint32_t idx;                         // input position (final tie-break, D-18)
 };
 
-__device__ __forceinline__ int bk_bucket(uint32_t keybits, float m0, float scale) {
-  const bool forced = (keybits >> 31) == 0u;
+struct BkParams {
+  float m0, scale;                      // L interval of bucket 0, buckets per unit of L
+  uint32_t tie_bits;                    // keybits of an unobserved request: !forced | E_pi[L]
+  int ustar;                            // L bucket of E_pi[L]
+};
+
+__device__ __forceinline__ int bk_lbucket(uint32_t keybits, const BkParams &bp) {
   const float L = __uint_as_float(keybits & 0x7FFFFFFFu);
-  float u = (L - m0) * scale;           // NaN/inf keys -> last bucket of the class
+  const float u = (L - bp.m0) * bp.scale;  // NaN/inf keys -> last bucket of the class
   int b = (u >= 0.f) ? (u < (float)kBH ? (int)u : kBH - 1) : 0;
   if (!(L == L) || L == INFINITY) b = kBH - 1;
-  return forced ? b : kBH + b;
+  return b;
+}
+
+// bucket of a (non-padding) record; tie = (~amin, amax) of the tie group's arrivals
+__device__ __forceinline__ int bk_bucket(uint32_t keybits, uint32_t arrival, const BkParams &bp,
+                                         uint32_t amin, uint32_t amax) {
+  const int u = bk_lbucket(keybits, bp);
+  if ((keybits >> 31) == 0u) return u;                                   // forced class
+  if (keybits == bp.tie_bits) {
+    const unsigned long long span = (unsigned long long)(amax - amin) + 1ull;
+    const unsigned long long sub = ((unsigned long long)(arrival - amin) * kTie) / span;
+    return kBH + bp.ustar + 1 + (int)(sub < (unsigned long long)kTie ? sub : kTie - 1);
+  }
+  if (u < bp.ustar) return kBH + u;
+  if (u > bp.ustar) return kBH + u + 1 + kTie;
+  return keybits < bp.tie_bits ? kBH + bp.ustar : kBH + bp.ustar + 1 + kTie;
 }
 
 __device__ __forceinline__ bool bk_less(const BkEntry &a, const BkEntry &b) {
@@ -63,13 +89,21 @@ struct BkScan {
 
 __device__ void bk_scan_buckets(BkScan &sh, const uint32_t *hcnt, const uint32_t *hrun,
                                 const unsigned long long *hkv) {
+  constexpr int PT = kB / kB3Threads;   // consecutive buckets per thread
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  // two buckets per thread: 2t, 2t+1
-  uint32_t c0 = __ldcg(hcnt + 2 * t), c1 = __ldcg(hcnt + 2 * t + 1);
-  uint32_t r0 = __ldcg(hrun + 2 * t), r1 = __ldcg(hrun + 2 * t + 1);
-  unsigned long long k0 = __ldcg(hkv + 2 * t), k1 = __ldcg(hkv + 2 * t + 1);
-  uint32_t ic = c0 + c1, ir = r0 + r1;
-  unsigned long long ik = k0 + k1;
+  uint32_t c[PT], r[PT];
+  unsigned long long k[PT];
+  uint32_t ic = 0, ir = 0;
+  unsigned long long ik = 0;
+#pragma unroll
+  for (int q = 0; q < PT; ++q) {
+    c[q] = __ldcg(hcnt + PT * t + q);
+    r[q] = __ldcg(hrun + PT * t + q);
+    k[q] = __ldcg(hkv + PT * t + q);
+    ic += c[q]; ir += r[q]; ik += k[q];
+  }
+  const uint32_t tc0 = ic, tr0 = ir;
+  const unsigned long long tk0 = ik;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t tc = __shfl_up_sync(0xffffffffu, ic, o), tr = __shfl_up_sync(0xffffffffu, ir, o);
@@ -92,44 +126,71 @@ __device__ void bk_scan_buckets(BkScan &sh, const uint32_t *hcnt, const uint32_t
     sh.wc[lane] = a - a0; sh.wr[lane] = b - b0; sh.wk[lane] = cc - cc0;
   }
   __syncthreads();
-  const uint32_t ec = sh.wc[w] + ic - (c0 + c1), er = sh.wr[w] + ir - (r0 + r1);
-  const unsigned long long ek = sh.wk[w] + ik - (k0 + k1);
-  sh.cnt[2 * t] = ec; sh.cnt[2 * t + 1] = ec + c0;
-  sh.run[2 * t] = er; sh.run[2 * t + 1] = er + r0;
-  sh.kv[2 * t] = ek; sh.kv[2 * t + 1] = ek + k0;
+  uint32_t ec = sh.wc[w] + ic - tc0, er = sh.wr[w] + ir - tr0;
+  unsigned long long ek = sh.wk[w] + ik - tk0;
+#pragma unroll
+  for (int q = 0; q < PT; ++q) {
+    sh.cnt[PT * t + q] = ec; sh.run[PT * t + q] = er; sh.kv[PT * t + q] = ek;
+    ec += c[q]; er += r[q]; ek += k[q];
+  }
   __syncthreads();
 }
 }  // namespace
 
-// B1: per-bucket totals
+// B0: records (local path) and the arrival range of the E_pi[L] tie group
 __global__ void __launch_bounds__(256)
-trail_bucket_hist_kernel(const Record *__restrict__ rec, Record *__restrict__ rec_out,
+trail_bucket_prep_kernel(const Record *__restrict__ rec, Record *__restrict__ rec_out,
                          const uint32_t *__restrict__ ids, const uint32_t *__restrict__ arrival,
                          const int32_t *__restrict__ kvin, const uint8_t *__restrict__ running,
                          const SlotMeta *__restrict__ meta, const HeadConsts *__restrict__ cst,
-                         int max_slots, uint32_t id_base, uint32_t *__restrict__ err,
-                         int m, float m0, float scale,
-                         uint32_t *__restrict__ hcnt, uint32_t *__restrict__ hrun,
-                         unsigned long long *__restrict__ hkv) {
+                         int max_slots, uint32_t id_base, uint32_t *__restrict__ err, int m,
+                         uint32_t tie_bits, uint32_t *__restrict__ tie) {
   griddep_wait();     // records from the pack kernel / the all-gather, or the slot state
   griddep_launch();
+  for (int i0 = blockIdx.x * blockDim.x; i0 < m; i0 += gridDim.x * blockDim.x) {
+    const int i = i0 + threadIdx.x;
+    uint32_t kb = kPadKey, arr = 0u;
+    if (i < m) {
+      if (rec) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(rec + i));
+        kb = v.x;
+        arr = v.y;
+      } else {        // local path: row a4 fused (the record build of trail_schedule_pack)
+        const Record r = build_record(__ldg(ids + i), __ldg(arrival + i), __ldg(kvin + i),
+                                      __ldg(running + i) != 0, meta, cst, max_slots, id_base, err);
+        rec_out[i] = r;
+        kb = r.keybits;
+        arr = r.arrival;
+      }
+    }
+    const bool t = kb == tie_bits;
+    const uint32_t mx = __reduce_max_sync(0xffffffffu, t ? arr : 0u);
+    const uint32_t nmn = __reduce_max_sync(0xffffffffu, t ? ~arr : 0u);
+    const bool any = __any_sync(0xffffffffu, t);          // every lane votes
+    if ((threadIdx.x & 31) == 0 && any) {
+      atomicMax(tie, nmn);          // ~min arrival
+      atomicMax(tie + 1, mx);       // max arrival
+    }
+  }
+}
+
+// B1: per-bucket totals
+__global__ void __launch_bounds__(256)
+trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, BkParams bp,
+                         const uint32_t *__restrict__ tie, uint32_t *__restrict__ hcnt,
+                         uint32_t *__restrict__ hrun, unsigned long long *__restrict__ hkv) {
+  griddep_wait();     // records and the tie range from B0
+  griddep_launch();
+  const uint32_t amin = ~__ldcg(tie), amax = __ldcg(tie + 1);
   const int lane = threadIdx.x & 31;
   for (int i0 = blockIdx.x * blockDim.x; i0 < m; i0 += gridDim.x * blockDim.x) {
     const int i = i0 + threadIdx.x;
     int b = -1;
     uint32_t kvv = 0, runn = 0;
     if (i < m) {
-      uint4 v;
-      if (rec) {
-        v = __ldg(reinterpret_cast<const uint4 *>(rec + i));
-      } else {        // local path: row a4 fused (the record build of trail_schedule_pack)
-        const Record r = build_record(__ldg(ids + i), __ldg(arrival + i), __ldg(kvin + i),
-                                      __ldg(running + i) != 0, meta, cst, max_slots, id_base, err);
-        rec_out[i] = r;
-        v = make_uint4(r.keybits, r.arrival, r.kv, r.gid);
-      }
+      const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(rec + i));
       if (v.x != kPadKey) {
-        b = bk_bucket(v.x, m0, scale);
+        b = bk_bucket(v.x, v.y, bp, amin, amax);
         kvv = v.z;
         runn = v.w >> 31;
       }
@@ -149,7 +210,8 @@ trail_bucket_hist_kernel(const Record *__restrict__ rec, Record *__restrict__ re
 
 // B2: scatter into bucket order
 __global__ void __launch_bounds__(kB3Threads)
-trail_bucket_scatter_kernel(const Record *__restrict__ rec, int m, float m0, float scale,
+trail_bucket_scatter_kernel(const Record *__restrict__ rec, int m, BkParams bp,
+                            const uint32_t *__restrict__ tie,
                             const uint32_t *__restrict__ hcnt, const uint32_t *__restrict__ hrun,
                             const unsigned long long *__restrict__ hkv,
                             uint32_t *__restrict__ cursor, BkEntry *__restrict__ sorted) {
@@ -158,14 +220,15 @@ trail_bucket_scatter_kernel(const Record *__restrict__ rec, int m, float m0, flo
   griddep_wait();
   griddep_launch();
   bk_scan_buckets(sh, hcnt, hrun, hkv);
+  const uint32_t amin = ~__ldcg(tie), amax = __ldcg(tie + 1);
   const int lane = threadIdx.x & 31;
   for (int i0 = blockIdx.x * blockDim.x; i0 < m; i0 += gridDim.x * blockDim.x) {
     const int i = i0 + threadIdx.x;
     int b = -1;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (i < m) {
-      v = __ldg(reinterpret_cast<const uint4 *>(rec + i));
-      if (v.x != kPadKey) b = bk_bucket(v.x, m0, scale);
+      v = __ldcg(reinterpret_cast<const uint4 *>(rec + i));
+      if (v.x != kPadKey) b = bk_bucket(v.x, v.y, bp, amin, amax);
     }
     const unsigned peers = __match_any_sync(0xffffffffu, b);
     const int leader = __ffs(peers) - 1;
@@ -185,7 +248,7 @@ trail_bucket_scatter_kernel(const Record *__restrict__ rec, int m, float m0, flo
 
 // B3: exact positions, cumulative KV, running-before; lists
 __global__ void __launch_bounds__(kB3Threads)
-trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, float m0, float scale,
+trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, uint32_t *__restrict__ tie,
                          uint32_t *__restrict__ hcnt,
                          uint32_t *__restrict__ hrun, unsigned long long *__restrict__ hkv,
                          uint32_t *__restrict__ cursor, const BkEntry *__restrict__ sorted,
@@ -241,7 +304,9 @@ trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, float m0, float 
   int bs = 0, be = 0, b = 0;
   if (have) {
     me = staged ? stage[p - lo] : sorted[p];
-    b = bk_bucket((uint32_t)(me.key >> 32), m0, scale);
+    int a = 0, z = kB - 1;           // my bucket: the last prefix <= p
+    while (a < z) { const int mid = (a + z + 1) >> 1; if ((int)sh.cnt[mid] <= p) a = mid; else z = mid - 1; }
+    b = a;
     bs = (int)sh.cnt[b];
     be = b + 1 < kB ? (int)sh.cnt[b + 1] : nv;
   }
@@ -297,6 +362,8 @@ trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, float m0, float 
   // re-arm the histogram and cursors for the next call (every CTA has finished with them)
   for (int q = t; q < kB; q += kB3Threads) { hcnt[q] = 0u; hrun[q] = 0u; hkv[q] = 0ull; cursor[q] = 0u; }
   if (t == 0) {
+    tie[0] = 0u;
+    tie[1] = 0u;
     counts[0] = n_run;
     counts[1] = R_total - R_cut;
     counts[2] = n_run - R_cut;
@@ -306,7 +373,7 @@ trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, float m0, float 
 
 // ------------------------------------------------------------------ host
 size_t bucket_workspace_bytes(int m_max) {
-  return (size_t)kB * (4 + 4 + 8 + 4) + 16 + (size_t)m_max * (sizeof(BkEntry) + sizeof(uint2));
+  return (size_t)kB * (4 + 4 + 8 + 4) + 16 + 16 + (size_t)m_max * (sizeof(BkEntry) + sizeof(uint2));
 }
 
 cudaError_t select_bucket_prepare() {
@@ -330,25 +397,39 @@ cudaError_t launch_select_bucket(const Ctx &c, const Record *rec_in, Record *rec
   uint32_t *hrun = hcnt + kB;
   uint32_t *cursor = hrun + kB;
   unsigned long long *gcnt = reinterpret_cast<unsigned long long *>(cursor + kB);
-  BkEntry *sorted = reinterpret_cast<BkEntry *>(reinterpret_cast<uint8_t *>(gcnt) + 16);
+  uint32_t *tie = reinterpret_cast<uint32_t *>(gcnt + 2);       // ~min, max arrival of the group
+  BkEntry *sorted = reinterpret_cast<BkEntry *>(reinterpret_cast<uint8_t *>(gcnt) + 32);
   uint2 *scratch = reinterpret_cast<uint2 *>(sorted + c.bk_cap);
   const HeadConsts &hc = c.host_consts;
-  const float m0 = hc.m[0], mk = hc.m[c.k - 1];
-  const float scale = mk > m0 ? (float)kBH / (mk - m0) : 0.f;
+  BkParams bp;
+  bp.m0 = hc.m[0];
+  const float mk = hc.m[c.k - 1];
+  bp.scale = mk > bp.m0 ? (float)kBH / (mk - bp.m0) : 0.f;
+  float pl = hc.prior_L;
+  uint32_t plb;
+  memcpy(&plb, &pl, 4);
+  bp.tie_bits = 0x80000000u | (plb & 0x7FFFFFFFu);
+  {
+    const float u = (pl - bp.m0) * bp.scale;
+    bp.ustar = (u >= 0.f) ? (u < (float)kBH ? (int)u : kBH - 1) : 0;
+  }
   const int g1 = std::max(1, std::min(2 * c.num_sms, (m + 255) / 256));
-  cudaError_t e = launch_k(trail_bucket_hist_kernel, dim3(g1), dim3(256), 0, s, rec_in, rec_out,
+  cudaError_t e = launch_k(trail_bucket_prep_kernel, dim3(g1), dim3(256), 0, s, rec_in, rec_out,
                            ids, arrival, kv, running, (const SlotMeta *)c.meta,
                            (const HeadConsts *)c.consts, c.cfg.max_slots, c.cfg.id_base,
-                           c.dev_err, m, m0, scale, hcnt, hrun, hkv);
+                           c.dev_err, m, bp.tie_bits, tie);
+  if (e != cudaSuccess) return e;
+  e = launch_k(trail_bucket_hist_kernel, dim3(g1), dim3(256), 0, s, rec, m, bp,
+               (const uint32_t *)tie, hcnt, hrun, hkv);
   if (e != cudaSuccess) return e;
   const int g2 = std::max(1, std::min(c.num_sms, (m + kB3Threads - 1) / kB3Threads));
   e = launch_k(trail_bucket_scatter_kernel, dim3(g2), dim3(kB3Threads), sizeof(BkScan), s, rec, m,
-               m0, scale, (const uint32_t *)hcnt, (const uint32_t *)hrun,
+               bp, (const uint32_t *)tie, (const uint32_t *)hcnt, (const uint32_t *)hrun,
                (const unsigned long long *)hkv, cursor, sorted);
   if (e != cudaSuccess) return e;
   const int g3 = std::max(1, (m + kB3Items - 1) / kB3Items);
   return launch_k(trail_bucket_rank_kernel, dim3(g3), dim3(kB3Threads),
-                  sizeof(BkScan) + kStageCap * sizeof(BkEntry), s, rec, m, m0, scale, hcnt, hrun, hkv,
+                  sizeof(BkScan) + kStageCap * sizeof(BkEntry), s, rec, m, tie, hcnt, hrun, hkv,
                   cursor, (const BkEntry *)sorted, (long long)budget, max_run, gcnt, scratch, run,
                   pre, adm, counts);
 }
