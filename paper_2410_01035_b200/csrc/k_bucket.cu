@@ -1,28 +1,32 @@
-// K4 (row a6) for large record counts (multi-rank all-gathers, configs 3-5): a bucketed
-// exact ranking in four PDL-chained kernels over the 16-byte records (row a4/a5).
+// K4 (row a6) for large record counts (multi-rank all-gathers, configs 3-5): a sample sort
+// in four PDL-chained kernels over the 16-byte records (row a4/a5).
 //
 // Same contract as every selection kernel: order = (keybits << 32 | arrival, input position)
 // ascending — forced first (rank -inf), then shortest predicted remaining length
 // (P:171), FCFS ties, then input position (D-18) — run set = all forced + the
 // longest prefix of the rest within the KV budget and run cap (strict prefix D-15, overflow
-// D-16).
+// D-16).  (key, input position) pairs are unique, so the order is a strict total order.
 //
-// The key of a record is L_t, a convex combination of the bin midpoints, so it lies in
-// [m_0, m_{k-1}] (create-time constants): buckets are equal-width L intervals (1024 for the
-// forced class, 1024 for the rest), a monotone map of the key.  One exact tie is systematic:
-// every never-observed request is keyed E_pi[L] (D-24), and a burst of arrivals puts thousands
-// of them on one key; their order is FCFS (arrival), so that key gets its own range of 1024
-// arrival sub-buckets between the lower and the upper part of its L interval.
-//   B0  (local path) the records (row a4, fused pack); arrival range of the E_pi[L] tie group
-//   B1  histogram of (count, KV, running) per bucket (warp-aggregated global atomics)
-//   B2  scatter of the records into bucket order (prefix of the counts, atomic cursors)
+// Bucket boundaries come from the data, not from the key range: the keys cluster — every
+// never-observed request is keyed E_pi[L] exactly (D-24), thousands of them in a burst of
+// arrivals, and posteriors that have collapsed onto one bin put their L at that bin's middle
+// to within ~1e-6 — so equal-width L buckets leave a few buckets with thousands of records
+// and an O(b^2) in-bucket ranking (measured: 49 us of a 65 us selection at configs[3] with
+// L buckets; 4.7 ms for an 81 920-record unseen burst).
+//   B0  1024 samples of (composite key, input position) on a jittered stride are ranked by
+//       counting (a warp per sample over the staged sample set); sample of rank r becomes
+//       splitter r - 1, so the 1023 splitters cut the records into 1024 buckets of about
+//       m / 1024 whatever the key distribution (a tie cluster is split by arrival like any
+//       other run of keys).  On the local path B0 also builds every record (row a4).
+//   B1  bucket of each record = binary search over the splitters (shared memory); histogram
+//       of (count, KV, running) per bucket + forced totals (warp-aggregated global atomics)
+//   B2  scatter of the records into bucket order (prefix of the counts, atomic cursors; the
+//       bucket ids B1 found are reused)
 //   B3  each record counts the records of its own bucket ordered before it (the bucket range
-//       is staged in shared memory; 16 threads per record), adds the bucket prefixes
+//       is staged in shared memory; 8 threads per record), adds the bucket prefixes
 //       -> position, cumulative KV, running-before, and the lists follow as in k_rank.cu
 //       (one packed acq_rel atomic; the last CTA writes the preempt list and re-arms).
-// Cost is O(m + sum over buckets of size^2 / 16).
-#include <string.h>
-
+// Cost is O(m log m + sum over buckets of size^2 / 8) with bucket sizes ~ m / 1024.
 #include <algorithm>
 
 #include "trail_internal.cuh"
@@ -30,15 +34,13 @@
 namespace trail {
 
 namespace {
-constexpr int kBH = 1024;               // L buckets per class (forced / not forced)
-constexpr int kTie = 1024;              // arrival sub-buckets of the E_pi[L] tie group
-constexpr int kBUsed = 2 * kBH + 1 + kTie;
-constexpr int kB = 4096;                // bucket slots (kBUsed rounded up; 4 per scan thread)
-static_assert(kBUsed <= kB, "bucket layout exceeds the scanned slots");
+constexpr int kB = 1024;                // buckets (= samples: every sample but the smallest
+constexpr int kS = kB;                  //  is a splitter)
+constexpr int kB0Threads = 1024;
 constexpr int kB3Threads = 1024;
-constexpr int kB3Tpi = 16;              // threads per record in B3
+constexpr int kB3Tpi = 8;               // threads per record in B3
 constexpr int kB3Items = kB3Threads / kB3Tpi;
-constexpr int kStageCap = 8192;         // bucket entries staged in shared memory (128 KB)
+constexpr int kStageCap = 4096;         // bucket entries staged in shared memory (64 KB)
 
 struct BkEntry {                        // bucket-sorted record (16 B)
   unsigned long long key;               // keybits << 32 | arrival
@@ -46,37 +48,35 @@ struct BkEntry {                        // bucket-sorted record (16 B)
   uint32_t idx;                         // input position (final tie-break, D-18)
 };
 
-struct BkParams {
-  float m0, scale;                      // L interval of bucket 0, buckets per unit of L
-  uint32_t tie_bits;                    // keybits of an unobserved request: !forced | E_pi[L]
-  int ustar;                            // L bucket of E_pi[L]
+struct __align__(16) BkKey {            // splitter / sample: (composite key, input position)
+  unsigned long long key;
+  uint32_t idx, pad;
 };
 
-__device__ __forceinline__ int bk_lbucket(uint32_t keybits, const BkParams &bp) {
-  const float L = __uint_as_float(keybits & 0x7FFFFFFFu);
-  const float u = (L - bp.m0) * bp.scale;  // NaN/inf keys -> last bucket of the class
-  int b = (u >= 0.f) ? (u < (float)kBH ? (int)u : kBH - 1) : 0;
-  if (!(L == L) || L == INFINITY) b = kBH - 1;
-  return b;
-}
-
-// bucket of a (non-padding) record; tie = (~amin, amax) of the tie group's arrivals
-__device__ __forceinline__ int bk_bucket(uint32_t keybits, uint32_t arrival, const BkParams &bp,
-                                         uint32_t amin, uint32_t amax) {
-  const int u = bk_lbucket(keybits, bp);
-  if ((keybits >> 31) == 0u) return u;                                   // forced class
-  if (keybits == bp.tie_bits) {
-    const unsigned long long span = (unsigned long long)(amax - amin) + 1ull;
-    const unsigned long long sub = ((unsigned long long)(arrival - amin) * kTie) / span;
-    return kBH + bp.ustar + 1 + (int)(sub < (unsigned long long)kTie ? sub : kTie - 1);
-  }
-  if (u < bp.ustar) return kBH + u;
-  if (u > bp.ustar) return kBH + u + 1 + kTie;
-  return keybits < bp.tie_bits ? kBH + bp.ustar : kBH + bp.ustar + 1 + kTie;
+__device__ __forceinline__ bool bk_lt(unsigned long long ka, uint32_t ia, unsigned long long kb,
+                                      uint32_t ib) {
+  return ka < kb || (ka == kb && ia < ib);
 }
 
 __device__ __forceinline__ bool bk_less(const BkEntry &a, const BkEntry &b) {
-  return a.key < b.key || (a.key == b.key && a.idx < b.idx);
+  return bk_lt(a.key, a.idx, b.key, b.idx);
+}
+
+// bucket = number of splitters <= (key, idx): binary search over kB - 1 splitters in smem
+__device__ __forceinline__ int bk_bucket(const BkKey *__restrict__ spl, unsigned long long key,
+                                         uint32_t idx) {
+  int lo = 0, hi = kB - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const BkKey sp = spl[mid];
+    if (!bk_lt(key, idx, sp.key, sp.idx)) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ unsigned long long rec_key(uint32_t keybits, uint32_t arrival) {
+  return keybits == kPadKey ? ~0ull : (((unsigned long long)keybits << 32) | arrival);
 }
 
 // exclusive scan of kB (u32 count, u32 run, u64 kv) bucket totals by a 1024-thread CTA
@@ -135,65 +135,93 @@ __device__ void bk_scan_buckets(BkScan &sh, const uint32_t *hcnt, const uint32_t
   }
   __syncthreads();
 }
+
+// sample j of kS: a jittered stride over the input positions
+__device__ __forceinline__ int bk_sample_pos(int j, int m) {
+  const long long lo = (long long)j * m / kS, hi = (long long)(j + 1) * m / kS;
+  const uint32_t h = (uint32_t)j * 2654435761u;
+  return (int)(lo + (hi > lo ? (long long)(h % (uint32_t)(hi - lo)) : 0));
+}
 }  // namespace
 
-// B0: records (local path) and the arrival range of the E_pi[L] tie group
-__global__ void __launch_bounds__(256)
-trail_bucket_prep_kernel(const Record *__restrict__ rec, Record *__restrict__ rec_out,
-                         const uint32_t *__restrict__ ids, const uint32_t *__restrict__ arrival,
-                         const int32_t *__restrict__ kvin, const uint8_t *__restrict__ running,
-                         const SlotMeta *__restrict__ meta, const HeadConsts *__restrict__ cst,
-                         int max_slots, uint32_t id_base, uint32_t *__restrict__ err, int m,
-                         uint32_t tie_bits, uint32_t *__restrict__ tie) {
+// B0: records (local path) + sample ranking -> splitters
+__global__ void __launch_bounds__(kB0Threads)
+trail_bucket_sample_kernel(const Record *__restrict__ rec, Record *__restrict__ rec_out,
+                           const uint32_t *__restrict__ ids, const uint32_t *__restrict__ arrival,
+                           const int32_t *__restrict__ kvin, const uint8_t *__restrict__ running,
+                           const SlotMeta *__restrict__ meta, const HeadConsts *__restrict__ cst,
+                           int max_slots, uint32_t id_base, uint32_t *__restrict__ err, int m,
+                           BkKey *__restrict__ spl) {
+  __shared__ BkKey smp[kS];                                   // 32 KB
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   griddep_wait();     // records from the pack kernel / the all-gather, or the slot state
   griddep_launch();
-  for (int i0 = blockIdx.x * blockDim.x; i0 < m; i0 += gridDim.x * blockDim.x) {
-    const int i = i0 + threadIdx.x;
-    uint32_t kb = kPadKey, arr = 0u;
-    if (i < m) {
-      if (rec) {
-        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(rec + i));
-        kb = v.x;
-        arr = v.y;
-      } else {        // local path: row a4 fused (the record build of trail_schedule_pack)
-        const Record r = build_record(__ldg(ids + i), __ldg(arrival + i), __ldg(kvin + i),
-                                      __ldg(running + i) != 0, meta, cst, max_slots, id_base, err);
-        rec_out[i] = r;
-        kb = r.keybits;
-        arr = r.arrival;
-      }
+  // local path: every record, grid-stride (row a4, the record build of trail_schedule_pack)
+  if (!rec)
+    for (int i = blockIdx.x * kB0Threads + t; i < m; i += gridDim.x * kB0Threads)
+      rec_out[i] = build_record(__ldg(ids + i), __ldg(arrival + i), __ldg(kvin + i),
+                                __ldg(running + i) != 0, meta, cst, max_slots, id_base, err);
+  // the kS sample keys (built from the inputs on the local path: no dependency on other CTAs)
+  for (int j = t; j < kS; j += kB0Threads) {
+    const int i = bk_sample_pos(j, m);
+    uint32_t kb, ar;
+    if (rec) {
+      const uint2 v = __ldg(reinterpret_cast<const uint2 *>(rec + i));
+      kb = v.x;
+      ar = v.y;
+    } else {
+      const Record r = build_record(__ldg(ids + i), __ldg(arrival + i), __ldg(kvin + i),
+                                    __ldg(running + i) != 0, meta, cst, max_slots, id_base, err);
+      kb = r.keybits;
+      ar = r.arrival;
     }
-    const bool t = kb == tie_bits;
-    const uint32_t mx = __reduce_max_sync(0xffffffffu, t ? arr : 0u);
-    const uint32_t nmn = __reduce_max_sync(0xffffffffu, t ? ~arr : 0u);
-    const bool any = __any_sync(0xffffffffu, t);          // every lane votes
-    if ((threadIdx.x & 31) == 0 && any) {
-      atomicMax(tie, nmn);          // ~min arrival
-      atomicMax(tie + 1, mx);       // max arrival
+    BkKey k;
+    k.key = rec_key(kb, ar);
+    k.idx = (uint32_t)i;
+    k.pad = 0u;
+    smp[j] = k;
+  }
+  __syncthreads();
+  // one warp per sample: its rank r among the samples; rank r >= 1 is splitter r - 1
+  for (int j = blockIdx.x * (kB0Threads / 32) + warp; j < kS; j += gridDim.x * (kB0Threads / 32)) {
+    const BkKey me = smp[j];
+    uint32_t cnt = 0;
+#pragma unroll 4
+    for (int q = lane; q < kS; q += 32) {
+      const BkKey o = smp[q];
+      cnt += bk_lt(o.key, o.idx, me.key, me.idx) ? 1u : 0u;
     }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0 && cnt > 0) spl[cnt - 1] = me;
   }
 }
 
-// B1: per-bucket totals
+// B1: per-bucket totals (+ forced count / KV)
 __global__ void __launch_bounds__(256)
-trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, BkParams bp,
-                         const uint32_t *__restrict__ tie, uint32_t *__restrict__ hcnt,
-                         uint32_t *__restrict__ hrun, unsigned long long *__restrict__ hkv) {
-  griddep_wait();     // records and the tie range from B0
+trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, const BkKey *__restrict__ spl_g,
+                         uint32_t *__restrict__ hcnt, uint32_t *__restrict__ hrun,
+                         unsigned long long *__restrict__ hkv,
+                         unsigned long long *__restrict__ forced_tot,
+                         uint16_t *__restrict__ bkid) {
+  __shared__ BkKey spl[kB];
+  griddep_wait();     // splitters (and local records) from B0
   griddep_launch();
-  const uint32_t amin = ~__ldcg(tie), amax = __ldcg(tie + 1);
+  for (int q = threadIdx.x; q < kB - 1; q += blockDim.x) spl[q] = spl_g[q];
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   for (int i0 = blockIdx.x * blockDim.x; i0 < m; i0 += gridDim.x * blockDim.x) {
     const int i = i0 + threadIdx.x;
     int b = -1;
-    uint32_t kvv = 0, runn = 0;
+    uint32_t kvv = 0, runn = 0, frc = 0;
     if (i < m) {
       const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(rec + i));
       if (v.x != kPadKey) {
-        b = bk_bucket(v.x, v.y, bp, amin, amax);
+        b = bk_bucket(spl, rec_key(v.x, v.y), (uint32_t)i);
         kvv = v.z;
         runn = v.w >> 31;
+        frc = (v.x >> 31) == 0u ? 1u : 0u;
       }
+      bkid[i] = (uint16_t)(b < 0 ? 0xFFFF : b);   // reused by B2 (no second search)
     }
     const unsigned peers = __match_any_sync(0xffffffffu, b);
     const uint32_t c = __popc(peers);
@@ -205,13 +233,19 @@ trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, BkParams bp,
       if (r) atomicAdd(hrun + b, r);
       atomicAdd(hkv + b, ((unsigned long long)khi << 16) + klo);
     }
+    // forced totals: count in the high 24 bits, KV in the low 40 (both far below the caps)
+    const uint32_t fc = __reduce_add_sync(0xffffffffu, frc);
+    const uint32_t flo = __reduce_add_sync(0xffffffffu, frc ? (kvv & 0xFFFFu) : 0u);
+    const uint32_t fhi = __reduce_add_sync(0xffffffffu, frc ? (kvv >> 16) : 0u);
+    if (lane == 0 && fc)
+      atomicAdd(forced_tot, ((unsigned long long)fc << 40) + ((unsigned long long)fhi << 16) + flo);
   }
 }
 
 // B2: scatter into bucket order
 __global__ void __launch_bounds__(kB3Threads)
-trail_bucket_scatter_kernel(const Record *__restrict__ rec, int m, BkParams bp,
-                            const uint32_t *__restrict__ tie,
+trail_bucket_scatter_kernel(const Record *__restrict__ rec, int m,
+                            const uint16_t *__restrict__ bkid,
                             const uint32_t *__restrict__ hcnt, const uint32_t *__restrict__ hrun,
                             const unsigned long long *__restrict__ hkv,
                             uint32_t *__restrict__ cursor, BkEntry *__restrict__ sorted) {
@@ -219,8 +253,7 @@ trail_bucket_scatter_kernel(const Record *__restrict__ rec, int m, BkParams bp,
   BkScan &sh = *reinterpret_cast<BkScan *>(bsm);
   griddep_wait();
   griddep_launch();
-  bk_scan_buckets(sh, hcnt, hrun, hkv);
-  const uint32_t amin = ~__ldcg(tie), amax = __ldcg(tie + 1);
+  bk_scan_buckets(sh, hcnt, hrun, hkv);       // (synchronises)
   const int lane = threadIdx.x & 31;
   for (int i0 = blockIdx.x * blockDim.x; i0 < m; i0 += gridDim.x * blockDim.x) {
     const int i = i0 + threadIdx.x;
@@ -228,7 +261,8 @@ trail_bucket_scatter_kernel(const Record *__restrict__ rec, int m, BkParams bp,
     uint4 v = make_uint4(0, 0, 0, 0);
     if (i < m) {
       v = __ldcg(reinterpret_cast<const uint4 *>(rec + i));
-      if (v.x != kPadKey) b = bk_bucket(v.x, v.y, bp, amin, amax);
+      const uint16_t bb = __ldcg(bkid + i);
+      b = bb == 0xFFFF ? -1 : (int)bb;
     }
     const unsigned peers = __match_any_sync(0xffffffffu, b);
     const int leader = __ffs(peers) - 1;
@@ -248,9 +282,9 @@ trail_bucket_scatter_kernel(const Record *__restrict__ rec, int m, BkParams bp,
 
 // B3: exact positions, cumulative KV, running-before; lists
 __global__ void __launch_bounds__(kB3Threads)
-trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, uint32_t *__restrict__ tie,
-                         uint32_t *__restrict__ hcnt,
+trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, uint32_t *__restrict__ hcnt,
                          uint32_t *__restrict__ hrun, unsigned long long *__restrict__ hkv,
+                         unsigned long long *__restrict__ forced_tot,
                          uint32_t *__restrict__ cursor, const BkEntry *__restrict__ sorted,
                          long long budget, int max_run, unsigned long long *__restrict__ gcnt,
                          uint2 *__restrict__ scratch, uint32_t *__restrict__ run_ids,
@@ -267,8 +301,9 @@ trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, uint32_t *__rest
   const int t = threadIdx.x;
   bk_scan_buckets(sh, hcnt, hrun, hkv);
   const int nv = (int)(sh.cnt[kB - 1] + __ldcg(hcnt + kB - 1));
-  const int nf = (int)sh.cnt[kBH];                 // forced records = the first class
-  const unsigned long long Sf = sh.kv[kBH];
+  const unsigned long long ft = __ldcg(forced_tot);
+  const int nf = (int)(ft >> 40);
+  const unsigned long long Sf = ft & ((1ull << 40) - 1);
   const int R_total = (int)(sh.run[kB - 1] + __ldcg(hrun + kB - 1));
   const int cap = max_run > 0 ? max_run : nv;
   const bool over = (long long)Sf > budget || nf > cap;
@@ -362,8 +397,7 @@ trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, uint32_t *__rest
   // re-arm the histogram and cursors for the next call (every CTA has finished with them)
   for (int q = t; q < kB; q += kB3Threads) { hcnt[q] = 0u; hrun[q] = 0u; hkv[q] = 0ull; cursor[q] = 0u; }
   if (t == 0) {
-    tie[0] = 0u;
-    tie[1] = 0u;
+    *forced_tot = 0ull;
     counts[0] = n_run;
     counts[1] = R_total - R_cut;
     counts[2] = n_run - R_cut;
@@ -373,12 +407,14 @@ trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, uint32_t *__rest
 
 // ------------------------------------------------------------------ host
 size_t bucket_workspace_bytes(int m_max) {
-  return (size_t)kB * (4 + 4 + 8 + 4) + 16 + 16 + (size_t)m_max * (sizeof(BkEntry) + sizeof(uint2));
+  return (size_t)kB * (4 + 4 + 8 + 4) + 16 + 16 + (size_t)kB * sizeof(BkKey) +
+         (size_t)m_max * (sizeof(BkEntry) + sizeof(uint2) + sizeof(uint16_t)) + 16;
 }
 
 cudaError_t select_bucket_prepare() {
   cudaError_t e = cudaFuncSetAttribute(trail_bucket_scatter_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BkScan));
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(BkScan));
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(trail_bucket_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(sizeof(BkScan) + kStageCap * sizeof(BkEntry)));
@@ -390,48 +426,40 @@ cudaError_t launch_select_bucket(const Ctx &c, const Record *rec_in, Record *rec
                                  int max_run, uint32_t *run, uint32_t *pre, uint32_t *adm,
                                  int32_t *counts, cudaStream_t s) {
   const Record *rec = rec_in ? rec_in : rec_out;
-  if (!c.bk_ws) return cudaErrorInvalidValue;
+  if (!c.bk_ws || m < kS) return cudaErrorInvalidValue;
   uint8_t *ws = reinterpret_cast<uint8_t *>(c.bk_ws);
   unsigned long long *hkv = reinterpret_cast<unsigned long long *>(ws);
   uint32_t *hcnt = reinterpret_cast<uint32_t *>(ws + (size_t)kB * 8);
   uint32_t *hrun = hcnt + kB;
   uint32_t *cursor = hrun + kB;
   unsigned long long *gcnt = reinterpret_cast<unsigned long long *>(cursor + kB);
-  uint32_t *tie = reinterpret_cast<uint32_t *>(gcnt + 2);       // ~min, max arrival of the group
-  BkEntry *sorted = reinterpret_cast<BkEntry *>(reinterpret_cast<uint8_t *>(gcnt) + 32);
+  unsigned long long *forced_tot = gcnt + 2;
+  BkKey *spl = reinterpret_cast<BkKey *>(forced_tot + 2);
+  BkEntry *sorted = reinterpret_cast<BkEntry *>(spl + kB);
   uint2 *scratch = reinterpret_cast<uint2 *>(sorted + c.bk_cap);
-  const HeadConsts &hc = c.host_consts;
-  BkParams bp;
-  bp.m0 = hc.m[0];
-  const float mk = hc.m[c.k - 1];
-  bp.scale = mk > bp.m0 ? (float)kBH / (mk - bp.m0) : 0.f;
-  float pl = hc.prior_L;
-  uint32_t plb;
-  memcpy(&plb, &pl, 4);
-  bp.tie_bits = 0x80000000u | (plb & 0x7FFFFFFFu);
-  {
-    const float u = (pl - bp.m0) * bp.scale;
-    bp.ustar = (u >= 0.f) ? (u < (float)kBH ? (int)u : kBH - 1) : 0;
-  }
-  const int g1 = std::max(1, std::min(2 * c.num_sms, (m + 255) / 256));
-  cudaError_t e = launch_k(trail_bucket_prep_kernel, dim3(g1), dim3(256), 0, s, rec_in, rec_out,
-                           ids, arrival, kv, running, (const SlotMeta *)c.meta,
+  uint16_t *bkid = reinterpret_cast<uint16_t *>(scratch + c.bk_cap);
+  // B0: enough CTAs to build the records (local path) and a warp per sample
+  const int g0 = std::max(kS / (kB0Threads / 32),
+                          rec_in ? 0 : std::min(c.num_sms, (m + kB0Threads - 1) / kB0Threads));
+  cudaError_t e = launch_k(trail_bucket_sample_kernel, dim3(g0), dim3(kB0Threads), 0, s, rec_in,
+                           rec_out, ids, arrival, kv, running, (const SlotMeta *)c.meta,
                            (const HeadConsts *)c.consts, c.cfg.max_slots, c.cfg.id_base,
-                           c.dev_err, m, bp.tie_bits, tie);
+                           c.dev_err, m, spl);
   if (e != cudaSuccess) return e;
-  e = launch_k(trail_bucket_hist_kernel, dim3(g1), dim3(256), 0, s, rec, m, bp,
-               (const uint32_t *)tie, hcnt, hrun, hkv);
+  const int g1 = std::max(1, std::min(2 * c.num_sms, (m + 255) / 256));
+  e = launch_k(trail_bucket_hist_kernel, dim3(g1), dim3(256), 0, s, rec, m, (const BkKey *)spl,
+               hcnt, hrun, hkv, forced_tot, bkid);
   if (e != cudaSuccess) return e;
   const int g2 = std::max(1, std::min(c.num_sms, (m + kB3Threads - 1) / kB3Threads));
   e = launch_k(trail_bucket_scatter_kernel, dim3(g2), dim3(kB3Threads), sizeof(BkScan), s, rec, m,
-               bp, (const uint32_t *)tie, (const uint32_t *)hcnt, (const uint32_t *)hrun,
+               (const uint16_t *)bkid, (const uint32_t *)hcnt, (const uint32_t *)hrun,
                (const unsigned long long *)hkv, cursor, sorted);
   if (e != cudaSuccess) return e;
   const int g3 = std::max(1, (m + kB3Items - 1) / kB3Items);
   return launch_k(trail_bucket_rank_kernel, dim3(g3), dim3(kB3Threads),
-                  sizeof(BkScan) + kStageCap * sizeof(BkEntry), s, rec, m, tie, hcnt, hrun, hkv,
-                  cursor, (const BkEntry *)sorted, (long long)budget, max_run, gcnt, scratch, run,
-                  pre, adm, counts);
+                  sizeof(BkScan) + kStageCap * sizeof(BkEntry), s, rec, m, hcnt, hrun, hkv,
+                  forced_tot, cursor, (const BkEntry *)sorted, (long long)budget, max_run, gcnt,
+                  scratch, run, pre, adm, counts);
 }
 
 }  // namespace trail

@@ -145,6 +145,17 @@ int main() {
              (double)wb * sms * g / (best * 1e-3) / 1e9);
     }
   }
+  // per-SM ingress with fewer CTAs (how many SMs does a pooling kernel need?)
+  for (int g : {20, 40, 74}) {
+    snprintf(nm, 64, "reg U=16 G=%d T=512", g);
+    run(nm, [&] { read_reg<16><<<g, 512>>>((const uint4 *)buf, bytes / 16, out); });
+    snprintf(nm, 64, "reg U=16 G=%d T=1024", g);
+    run(nm, [&] { read_reg<16><<<g, 1024>>>((const uint4 *)buf, bytes / 16, out); });
+    snprintf(nm, 64, "bulk NS=6 SB=32K G=%d", g);
+    run(nm, [&] { read_bulk<<<g, 256, 6 * 32768 + 16 * 6>>>(buf, bytes, 6, 32768, out); });
+    snprintf(nm, 64, "bulk NS=3 SB=64K G=%d", g);
+    run(nm, [&] { read_bulk<<<g, 256, 3 * 65536 + 16 * 3>>>(buf, bytes, 3, 65536, out); });
+  }
   run("cudaMemcpy D2D (r+w bytes/2)", [&] { cudaMemcpyAsync(flush, buf, bytes, cudaMemcpyDeviceToDevice); });
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
