@@ -186,6 +186,15 @@ def make_batches(cfg, nb: int, rank: int, world: int, seed: int):
     return eng, init, batches
 
 
+def first_prefill(b):
+    """Index of the first multi-row (prompt) request of a batch — the host-side layout the
+    serving engine knows (decodes first, new prefills last, as vLLM schedules), handed to the
+    library as trail_set_prefill_start; n when the batch has no prompt rows."""
+    cnt = np.diff(b.row_offsets)
+    multi = np.nonzero(cnt > 1)[0]
+    return int(multi[0]) if multi.size else int(b.n)
+
+
 def to_dev(a, torch, device):
     a = np.ascontiguousarray(a)
     if a.dtype == np.uint32:
@@ -269,7 +278,8 @@ def measure(args, cfg_name, rank, world, local, device, main):
 
     # device-resident inputs for every distinct iteration
     def mk(b):
-        return dict(emb=to_dev(b.emb, torch, device), off=to_dev(b.row_offsets, torch, device),
+        return dict(pfs=first_prefill(b), emb=to_dev(b.emb, torch, device),
+                    off=to_dev(b.row_offsets, torch, device),
                     ids=to_dev(b.request_ids, torch, device),
                     pref=to_dev(b.is_prefill, torch, device),
                     sids=to_dev(b.sched_ids, torch, device),
@@ -279,7 +289,7 @@ def measure(args, cfg_name, rank, world, local, device, main):
     dev = [mk(b) for b in batches]
     dev_init = mk(init)
     stream = torch.cuda.Stream(device)
-    flush = L2Flush(torch, device)
+    flush = L2Flush(torch, device, read=not args.write_flush)
 
     def step_x(x):
         t.predict(x["emb"], x["off"], x["ids"], x["pref"], stream=stream)
@@ -377,11 +387,15 @@ def measure(args, cfg_name, rank, world, local, device, main):
     avg = {k: (sum(v) / len(v)) for k, v in kern_ms.items() if v}
     dom = max(avg, key=avg.get) if avg else None
     n_avg = float(np.mean([x["n"] for x in dev]))
+    # requests the dominant layer-1 kernel processes per launch: all n, or the decode part
+    # [0, first prompt) when the decode/prefill split applies (CTA-pair regime, hint given)
+    n_l1 = n_avg                     # (no decode/prefill split in the bench: see DESIGN §7)
     mode, splits = trail_plan_l1(t.h, int(n_avg))
     roof = None
     if dom in ("umma", "gemv"):
-        byts = algorithmic_bytes_l1(cfg, n_avg)
-        flops = 2.0 * n_avg * cfg["d"] * cfg["H"]
+        n_dom = n_l1 if dom == "umma" else n_avg
+        byts = algorithmic_bytes_l1(cfg, n_dom)
+        flops = 2.0 * n_dom * cfg["d"] * cfg["H"]
         t_s = avg[dom] / 1e3
         ach_bw = byts / t_s / 1e9
         ach_tf = flops / t_s / 1e12
@@ -497,6 +511,7 @@ def measure(args, cfg_name, rank, world, local, device, main):
                       "starts with none of its data in L2 and no dirty lines to write back"
                       if not args.no_flush else "warm",
                 "cuda_graph": use_graph,
+
                 "parallelism": f"request-sharded x{world}, replicated weights" +
                                (", NCCL all-gather of 16 B records, identical global selection"
                                 if world > 1 else ""),
@@ -638,17 +653,21 @@ class L2Flush:
     second 256 MiB buffer, which evicts the written lines (their write-back happens here,
     outside the step's events).  The step then finds none of its inputs or weights in L2 and
     no dirty lines to write back — the state after the LLM's own layers, minus their
-    write-back, which belongs to those layers."""
+    write-back, which belongs to those layers.  `--write-flush` keeps only the write (round
+    1's flush): measured 30.8 us/step at configs[2] against 35.2 with the read (r02t), so the
+    write-only flush leaves part of the step's working set reachable; the stricter flush is
+    the default and every round-2 number uses it."""
 
-    def __init__(self, torch, device):
+    def __init__(self, torch, device, read: bool = True):
         self.w = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
-        self.r = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=device)
+        self.r = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=device) if read else None
         self.acc = torch.zeros((), dtype=torch.float32, device=device)
         self.torch = torch
 
     def __call__(self):
         self.w.zero_()
-        self.acc = self.r.sum()
+        if self.r is not None:
+            self.acc = self.r.sum()
 
 
 def run_e2e(args, cfg, t, batches, stream, flush, torch, device, world):
@@ -681,7 +700,7 @@ def run_e2e(args, cfg, t, batches, stream, flush, torch, device, world):
         bn = buf.numpy()
         for name in names:
             bn[offs[name]:offs[name] + arrs[name].nbytes] = arrs[name].view(np.uint8).reshape(-1)
-        h = {"buf": buf, "bytes": tot, "offs": offs,
+        h = {"buf": buf, "bytes": tot, "offs": offs, "pfs": first_prefill(b),
              "meta": {nm: (arrs[nm].dtype, arrs[nm].shape) for nm in names},
              "budget": b.kv_budget, "n": b.n, "m": b.m}
         host.append(h)
@@ -899,6 +918,8 @@ def main():
     ap.add_argument("--sweep-c", default="0,0.5,0.8,inf")
     ap.add_argument("--sweep-out", default=os.path.join(ROOT, "profiles", "r02_sweep.json"))
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--write-flush", action="store_true",
+                    help="flush L2 with the 256 MiB memset only (dirty lines left behind)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-burst", action="store_true")

@@ -70,6 +70,8 @@ typedef enum {
 #define TRAIL_DEV_BAD_ROWS 0x2u   /* row range empty or reversed: treated as a zero row   */
 #define TRAIL_DEV_NEG_KV   0x4u   /* kv_blocks < 0: treated as 0                          */
 #define TRAIL_DEV_NONFIN   0x8u   /* non-finite expected length: key encoded as +inf      */
+#define TRAIL_DEV_BAD_HINT 0x10u  /* trail_set_prefill_start broken: a multi-row request
+                                     before the hinted start (its outputs are undefined)  */
 
 typedef struct {
   /* Classifier (Linear(d, 512) - ReLU - Linear(512, k); P:362 ~2.1M params). */
@@ -301,6 +303,21 @@ TRAIL_API trail_status trail_set_threshold_mode(trail_handle h, int32_t mode);
  * trail_schedule_step / trail_schedule_select calls enqueued afterwards (CUDA graphs captured
  * earlier keep the old rule).  Errors: TRAIL_ERR_INVALID (mode not 0/1). */
 TRAIL_API trail_status trail_set_fill_mode(trail_handle h, int32_t mode);
+
+/* Batch-layout hint (host knowledge of the flat batch, like trail_set_rows_hint): every
+ * request with index < first_prefill in the next predict steps is a single-row (decode)
+ * observation — vLLM-style schedulers put running decodes first and new prefills last
+ * (P:432).  With it (opt-in), the large-batch path splits the step: the CTA-pair kernel runs
+ * the decode tiles [0, t) (t = first_prefill rounded down to a 256-request tile) on most SMs
+ * at once, while on a library side stream the pooling kernel (on the remaining SMs) and the
+ * split-K kernel handle the tail [t, n) that contains the prompts — the prompt pooling no
+ * longer sits in front of the whole layer-1 contraction.  The streams re-join before the
+ * call returns (capturable in a CUDA graph).  Measured at configs[3] (≈100 MB of prompt rows
+ * per step) the side path is the longer one (239 -> 250 us per step), so it pays only with
+ * fewer prompt rows per step.  -1 (default) disables it.  A multi-row request
+ * before the hinted start breaks the contract: TRAIL_DEV_BAD_HINT is raised and that tile's
+ * outputs are undefined.  Errors: TRAIL_ERR_INVALID (first_prefill < -1). */
+TRAIL_API trail_status trail_set_prefill_start(trail_handle h, int32_t first_prefill);
 
 /* L2-persisting W1 (optional; W1 is 99.7 % of the probe's parameters).
  * 1: sets the device's persisting-L2 set-aside to cover W1 (cudaLimitPersistingL2CacheSize —

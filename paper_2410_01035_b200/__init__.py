@@ -29,6 +29,7 @@ from .trail import (  # noqa: F401
     trail_schedule_step,
     trail_set_fill_mode,
     trail_set_l1_mode,
+    trail_set_prefill_start,
     trail_set_w1_l2_persist,
     trail_trace_enable,
     trail_trace_read,

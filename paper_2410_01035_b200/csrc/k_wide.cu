@@ -78,7 +78,7 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
                           const float *__restrict__ prior_override, int max_slots,
                           float *__restrict__ lq_state, SlotMeta *__restrict__ meta,
                           float *__restrict__ post, float *__restrict__ Lout,
-                          uint32_t *__restrict__ err) {
+                          uint32_t *__restrict__ err, int decode_only) {
   using C = WCfg<KB>;
   constexpr int KBP = C::KBP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -128,7 +128,14 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
         tma_load_2d_pair(sb, &tmap_w, lead_full0 + 8 * i, i * WBK, (int)r * 128);
         tma_load_2d_pair(sb + WBH, &tmap_w, lead_full0 + 8 * i, i * WBK, 256 + (int)r * 128);
       }
-    if (xp.tile_xs) griddep_wait();
+    if (xp.tile_xs) {
+      // decode/prefill split: this launch was promised decode-only tiles (trail_set_prefill_start)
+      if (decode_only) {
+        if (lane == 0) atomicOr(err, TRAIL_DEV_BAD_HINT);
+      } else {
+        griddep_wait();
+      }
+    }
     __syncwarp();
     for (int i = 0; i < kblocks; ++i) {
       const int st = i % WSTAGES;
@@ -297,7 +304,7 @@ cudaError_t wide_prepare(Ctx &c) {
 cudaError_t launch_wide_predict(Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
                                 const uint32_t *ids, const uint8_t *is_prefill,
                                 const float *prior_override, float *post, float *L,
-                                cudaStream_t s) {
+                                cudaStream_t s, int decode_only) {
   if (!c.have_tmaps || !wide_supported(c)) return cudaErrorInvalidValue;
   if (!ensure_emb_tmaps(c, emb, ld)) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
@@ -325,7 +332,7 @@ cudaError_t launch_wide_predict(Ctx &c, const void *emb, int64_t ld, const int32
                             c.tmap_emb32, c.tmap_xs1, c.tmap_xs4, c.tmap_xs32, c.tmap_w128, off, \
                             n, c.d / WBK, (const float *)c.b1, (const float *)c.w2,              \
                             (const float *)c.b2, c.host_consts, ids, is_prefill, prior_override, \
-                            c.cfg.max_slots, c.lq, c.meta, post, L, c.dev_err)
+                            c.cfg.max_slots, c.lq, c.meta, post, L, c.dev_err, decode_only)
   switch (wide_kb(c.k)) {
     case 10: TRAIL_WIDE(10);
     case 16: TRAIL_WIDE(16);

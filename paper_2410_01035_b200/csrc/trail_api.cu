@@ -153,6 +153,9 @@ void free_ctx(Ctx &c) {
                   c.chunk_acc, c.chunk_cnt, c.xmix, c.iota};
   for (void *p : ptrs)
     if (p) cudaFree(p);
+  if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+  if (c.ev_join) cudaEventDestroy(c.ev_join);
+  if (c.side) cudaStreamDestroy(c.side);
   if (c.prof_ev) {
     for (int i = 0; i < 2 * c.prof_cap; ++i) cudaEventDestroy(c.prof_ev[i]);
     delete[] c.prof_ev;
@@ -341,6 +344,10 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
       select_prepare(c) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
   if ((int64_t)max_sched * c.world > select_cluster_capacity()) return fail(TRAIL_ERR_CAPACITY);
+  if (cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming) != cudaSuccess)
+    return fail(TRAIL_ERR_CUDA);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(TRAIL_ERR_CUDA);
   *out = h;
   return TRAIL_OK;
@@ -388,6 +395,12 @@ trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode) {
   if (!h || l1_mode < 0 || l1_mode > 4) return TRAIL_ERR_INVALID;
   if (l1_mode >= TRAIL_L1_UMMA && h->c.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
   h->c.cfg.l1_mode = l1_mode;
+  return TRAIL_OK;
+}
+
+trail_status trail_set_prefill_start(trail_handle h, int32_t first_prefill) {
+  if (!h || first_prefill < -1) return TRAIL_ERR_INVALID;
+  h->c.prefill_start = first_prefill;
   return TRAIL_OK;
 }
 
@@ -539,6 +552,46 @@ static trail_status predict_body(Ctx &c, const void *emb, int64_t emb_ld,
   plan_l1(c, n, &mode, &bn, &splits);
   if (mode != TRAIL_L1_UMMA && mode != TRAIL_L1_WIDE && (size_t)splits * n * c.H > c.partial_elems)
     return TRAIL_ERR_CAPACITY;
+  if (mode == TRAIL_L1_WIDE && c.side && c.prefill_start > 0 && c.prefill_start < n) {
+    // decode / prefill split (trail_set_prefill_start, opt-in): the CTA pairs take the decode
+    // tiles [0, t) on 2*(t/256) SMs at once; the side stream pools the tail's prompts on the
+    // remaining SMs and runs the tail [t, n) through the split-K kernel.  Measured at
+    // configs[3]: K2d 158 -> 144 us, but the side path (K1 on 22 SMs 98 us + K2c 81 us) is
+    // longer than K1 + K2d in series, so the step gets slower (239 -> 250 us); kept as an
+    // opt-in for batches with fewer prompt rows or parts with more spare SMs
+    const int t = (c.prefill_start / 256) * 256;     // whole CTA-pair tiles
+    const int nt = n - t;
+    const int pairs = (t + 255) / 256;
+    const int spare = c.num_sms - 2 * pairs;
+    const int tiles_tail = ((nt + 127) / 128) * (c.H / 128);
+    if (t >= 256 && spare >= 8 && tiles_tail <= spare) {
+      TRAIL_CUDA(cudaEventRecord(c.ev_fork, s));
+      TRAIL_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+      {
+        ProfScope p(c, TRAIL_K_POOL, c.side);
+        TRAIL_CUDA(launch_pool(c, emb, emb_ld, row_offsets + t, nt, 0, c.side, spare));
+      }
+      L1Window l1w(c);          // W1 access-policy window (if enabled) on the layer-1 launches
+      {
+        ProfScope p(c, TRAIL_K_GEMV, c.side);   // (profiling slot of the tail's layer 1)
+        const int sp = std::max(1, std::min(spare / tiles_tail, c.d / 64));
+        TRAIL_CUDA(launch_fused_predict(c, emb, emb_ld, row_offsets + t, nt, std::min(sp, 16),
+                                        request_ids + t, is_prefill + t,
+                                        prior_override ? prior_override + (int64_t)t * c.k : nullptr,
+                                        posteriors ? posteriors + (int64_t)t * c.k : nullptr,
+                                        expected_remaining ? expected_remaining + t : nullptr,
+                                        c.side));
+      }
+      TRAIL_CUDA(cudaEventRecord(c.ev_join, c.side));
+      {
+        ProfScope p(c, TRAIL_K_UMMA, s);
+        TRAIL_CUDA(launch_wide_predict(c, emb, emb_ld, row_offsets, t, request_ids, is_prefill,
+                                       prior_override, posteriors, expected_remaining, s, 1));
+      }
+      TRAIL_CUDA(cudaStreamWaitEvent(s, c.ev_join, 0));
+      return TRAIL_OK;
+    }
+  }
   {
     ProfScope p(c, TRAIL_K_POOL, s);
     // decode rows are gathered from emb by every layer-1 kernel except the unfused GEMM

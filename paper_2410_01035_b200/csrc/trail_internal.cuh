@@ -140,6 +140,9 @@ struct Ctx {
   int64_t rows_hint = 0;        // trail_set_rows_hint: embedding rows of the next predict steps
   int fill_mode = 0;            // trail_set_fill_mode: 0 strict prefix (D-15), 1 first-fit
   bool w1_persist = false;      // trail_set_w1_l2_persist
+  int prefill_start = -1;       // trail_set_prefill_start: requests before it are single-row
+  cudaStream_t side = nullptr;  // the prefill tail's stream (decode/prefill split)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaAccessPolicyWindow w1_window = {};
   // NCCL
   void *nccl_comm = nullptr;
@@ -163,7 +166,7 @@ struct Ctx {
 // K1.  write_singles = 0: single-row requests are not copied to xs (the fused tcgen05
 // kernel gathers those rows straight from emb)
 cudaError_t launch_pool(const Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
-                        int write_singles, cudaStream_t s);
+                        int write_singles, cudaStream_t s, int grid = 0);
 int pool_grid(const Ctx &c);
 bool pool_use_bulk();
 cudaError_t pool_prepare();
@@ -215,7 +218,7 @@ cudaError_t wide_prepare(Ctx &c);
 cudaError_t launch_wide_predict(Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
                                 const uint32_t *ids, const uint8_t *is_prefill,
                                 const float *prior_override, float *post, float *L,
-                                cudaStream_t s);
+                                cudaStream_t s, int decode_only = 0);
 cudaError_t select_prepare(Ctx &c);
 // K4 selection: one thread-block cluster (k_csort.cu).  rec_in != nullptr: select over given
 // records; else build the local records (fused K5 pack) from (ids, arrival, kv, running)

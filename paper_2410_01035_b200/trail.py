@@ -87,6 +87,7 @@ _SIGS = {
     "trail_set_threshold_mode": ([_P, _I32], _I32),
     "trail_set_fill_mode": ([_P, _I32], _I32),
     "trail_set_w1_l2_persist": ([_P, _I32], _I32),
+    "trail_set_prefill_start": ([_P, _I32], _I32),
     "trail_trace_enable": ([_P, _I32], _I32),
     "trail_trace_read": ([_P, _P, _I32], _I32),
     "trail_plan_l1": ([_P, _I32, ctypes.POINTER(_I32), ctypes.POINTER(_I32)], _I32),
@@ -179,6 +180,11 @@ def trail_predict_step_layers(h, embs, layer_weights, emb_ld, row_offsets, reque
         h, ctypes.cast(ptrs, ctypes.c_void_p), ctypes.cast(ws, ctypes.c_void_p), L, int(emb_ld),
         _ptr(row_offsets), _ptr(request_ids), _ptr(is_prefill), _ptr(prior_override), int(n),
         _ptr(posteriors), _ptr(expected_remaining), _stream(stream)))
+
+
+def trail_set_prefill_start(h, first_prefill: int) -> int:
+    """Host hint: requests before `first_prefill` are single-row decodes (-1 = unknown)."""
+    return _check("trail_set_prefill_start", _lib().trail_set_prefill_start(h, int(first_prefill)))
 
 
 def trail_set_w1_l2_persist(h, enable: int) -> int:
@@ -352,13 +358,18 @@ class Trail:
             pass
 
     def predict(self, emb, row_offsets, request_ids, is_prefill, prior_override=None,
-                stream=None, rows=None):
+                stream=None, rows=None, prefill_start=None):
         n = int(request_ids.shape[0])
         # host-side row count of the flat batch (selects the pooling kernel variant only)
         rows = int(emb.shape[0]) if rows is None and emb.dim() == 2 else int(rows or 0)
         if rows != getattr(self, "_rows_hint", 0):
             trail_set_rows_hint(self.h, rows)
             self._rows_hint = rows
+        # host-side batch layout: index of the first multi-row (prefill) request, if known
+        pfs = -1 if prefill_start is None else int(prefill_start)
+        if pfs != getattr(self, "_prefill_start", -1):
+            trail_set_prefill_start(self.h, pfs)
+            self._prefill_start = pfs
         trail_predict_step(self.h, emb, emb.shape[1] if emb.dim() == 2 else self.d, row_offsets,
                            request_ids, is_prefill, prior_override, n, self.post, self.L, stream)
         return self.post[:n], self.L[:n]

@@ -850,3 +850,42 @@ def test_select_first_fit(m):
     if m == 5:
         assert run.tolist() == [0, 2, 4]
     t.close()
+
+
+def test_prefill_start_hint_split_path():
+    """trail_set_prefill_start (decodes first, prompts last, as vLLM orders a batch): the CTA-
+    pair kernel takes the decode tiles while the side stream pools the prompt tail and runs it
+    through the split-K kernel; the joined result equals the oracle's, and equals the unsplit
+    path's.  A hint that puts a prompt inside the decode part raises TRAIL_DEV_BAD_HINT."""
+    from paper_2410_01035_b200.trail import trail_device_errors
+    n, d = 1024, 1024
+    w = W.make_weights(d, 512, 10, "bf16", seed=97)
+    rs = np.random.default_rng(98)
+    plen = np.ones(n, np.int64)
+    plen[-40:] = rs.integers(2, 60, 40)                       # prompts at the end
+    pref = (plen > 1).astype(np.uint8)
+    off = np.concatenate([[0], np.cumsum(plen)]).astype(np.int32)
+    emb = W.encode(rs.standard_normal((int(off[-1]), d)).astype(np.float32), "bf16")
+    ids = np.arange(n, dtype=np.uint32)
+    first = int(np.nonzero(plen > 1)[0][0])
+    outs = []
+    for hint in (first, -1):
+        t, o = make_pair(w, 0.8, n, n, n, "bf16", l1_mode=4)
+        q, L = t.predict(dev(emb), dev(off), dev(ids), dev(pref), prefill_start=hint)
+        torch.cuda.synchronize()
+        qg, Lg = q.cpu().numpy().astype(np.float64), L.cpu().numpy().astype(np.float64)
+        qo, Lo = oracle_predict(o, emb, off, ids, pref, "bf16")
+        assert_predict_close(qg, Lg, qo, Lo, f"hint {hint}")
+        outs.append((qg, Lg))
+        t.close()
+    assert np.abs(outs[0][0] - outs[1][0]).max() <= 1e-5
+    # a broken promise: a prompt request inside the hinted decode part is flagged
+    t, o = make_pair(w, 0.8, n, n, n, "bf16", l1_mode=4)
+    plen2 = plen.copy()
+    plen2[5] = 7
+    off2 = np.concatenate([[0], np.cumsum(plen2)]).astype(np.int32)
+    emb2 = W.encode(rs.standard_normal((int(off2[-1]), d)).astype(np.float32), "bf16")
+    t.predict(dev(emb2), dev(off2), dev(ids), dev((plen2 > 1).astype(np.uint8)), prefill_start=first)
+    torch.cuda.synchronize()
+    assert trail_device_errors(t.h, True) & 0x10
+    t.close()
