@@ -12,10 +12,17 @@
 // W1 rows {128r .. 128r+127} and {256 + 128r .. 256 + 128r + 127} (its halves of the two
 // N = 256 MMAs) — 48 KB per 64-wide K block — and the even CTA issues two M = 256, N = 256,
 // K = 16 MMAs per 16 columns of K for both.  X is read from HBM exactly once.
-//   warp 0        : TMA producer (X gather shared with K2c, xgather.cuh; W1 2 x 128 x 64)
-//                   — cta_group::2 loads completing on the LEADER's full barrier
-//   warp 1, even  : MMA issuer; tcgen05.commit multicast frees the stage in both CTAs
-//   warps 2-7     : stage b1, head constants and the slot state of the CTA's 128 rows
+//   warp 0        : X producer (row gather shared with K2c, xgather.cuh) into the X ring
+//                   (XS x 16 KB) — cta_group::2 loads completing on the LEADER's barrier
+//   warp 2        : W1 producer (2 x 128 x 64 per K block) into the W1 ring (WS x 32 KB)
+//   warp 1, even  : MMA issuer; tcgen05.commit multicast frees both rings' stages in both CTAs
+//   warps 3-7     : stage b1, head constants and the slot state of the CTA's 128 rows
+// Separate rings because the two operands behave differently (scripts/wide_probe.py,
+// configs[3], L2 flushed): the MMAs alone take 136 us, + the L2-resident W1 loads 138 us,
+// + the cold X rows from HBM 183 us with one shared 4 x 48 KB ring — X needs the deeper
+// buffer (7 x 16 KB: 191 -> 179 us per launch).  Deeper or batched X requests (8 stages,
+// 4 K blocks per request group) and L2 prefetch of the X rows ahead of the ring were
+// measured slower.
 //   all 8 warps   : epilogue — TMEM (lane = row) -> +b1, ReLU -> layer-2 partials over two
 //                   column halves (fixed order) -> head, one lane per bin (head_dev.cuh)
 #include <math.h>
@@ -39,14 +46,14 @@ constexpr int WBK = 64;
 constexpr int WH = 512;                        // hidden width held in TMEM (fp32 columns)
 constexpr int WA = WBM * WBK * 2;              // 16 KB: my 128 rows of X
 constexpr int WBH = 128 * WBK * 2;             // 16 KB: my 128 rows of one N half of W1
-constexpr int WSTAGE = WA + 2 * WBH;           // 48 KB per CTA per K block
-constexpr int WSTAGES = 4;
+constexpr int WS = 3;                          // W1 ring stages (2 x 16 KB each; L2-resident)
 
 template <int KB>
 struct WCfg {
   static constexpr int KBP = (KB + 3) & ~3;    // layer-2 bins padded to float4
-  static constexpr int PIPE = WSTAGES * WSTAGE;
-  static constexpr int BAR_OFF = PIPE;         // full[4], empty[4], done, tmem slot
+  static constexpr int XS = KB <= 20 ? 7 : 6;  // X ring stages (16 KB each)
+  static constexpr int PIPE = XS * WA + WS * 2 * WBH;
+  static constexpr int BAR_OFF = PIPE;         // xfull, xempty, wfull, wempty, done, tmem slot
   static constexpr int B1_OFF = BAR_OFF + 256;
   static constexpr int SLOT_OFF = B1_OFF + WH * 4;
   static constexpr int META_OFF = SLOT_OFF + WBM * 4;
@@ -78,14 +85,18 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
                           const float *__restrict__ prior_override, int max_slots,
                           float *__restrict__ lq_state, SlotMeta *__restrict__ meta,
                           float *__restrict__ post, float *__restrict__ Lout,
-                          uint32_t *__restrict__ err, int decode_only) {
+                          uint32_t *__restrict__ err, int decode_only, int wflags) {
   using C = WCfg<KB>;
   constexpr int KBP = C::KBP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t s0 = smem_u32(smem);
-  const uint32_t full0 = s0 + C::BAR_OFF, empty0 = full0 + 8 * WSTAGES, done = full0 + 16 * WSTAGES;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::BAR_OFF + 16 * WSTAGES + 8);
+  constexpr int XS = C::XS;
+  const uint32_t xfull0 = s0 + C::BAR_OFF, xempty0 = xfull0 + 8 * XS;
+  const uint32_t wfull0 = xempty0 + 8 * XS, wempty0 = wfull0 + 8 * WS, done = wempty0 + 8 * WS;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::BAR_OFF + 8 * (2 * XS + 2 * WS + 1));
+  // wflags bits 8/9: diagnostics that skip the X / W1 loads (wrong results; probes only)
+  const bool skip_x = (wflags & 0x100) != 0, skip_w = (wflags & 0x200) != 0;
   float *b1s = reinterpret_cast<float *>(smem + C::B1_OFF);
   uint32_t *s_slot = reinterpret_cast<uint32_t *>(smem + C::SLOT_OFF);
   SlotMeta *s_meta = reinterpret_cast<SlotMeta *>(smem + C::META_OFF);
@@ -100,9 +111,13 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
   const int k = cst.k;
 
   if (tid == 0) {
-    for (int i = 0; i < WSTAGES; ++i) {
-      mbar_init(full0 + 8 * i, 1);
-      mbar_init(empty0 + 8 * i, 1);
+    for (int i = 0; i < XS; ++i) {
+      mbar_init(xfull0 + 8 * i, 1);
+      mbar_init(xempty0 + 8 * i, 1);
+    }
+    for (int i = 0; i < WS; ++i) {
+      mbar_init(wfull0 + 8 * i, 1);
+      mbar_init(wempty0 + 8 * i, 1);
     }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -117,17 +132,13 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
   griddep_launch();
 
   if (warp == 0) {
+    // ---- X producer (all lanes: the row gather of xgather.cuh) into the X ring.  X streams
+    // from HBM once (cold rows), W1 from L2 (shared by every pair): measured alone, the MMAs
+    // take 136 us at configs[3], + W1 loads 138, + X loads 183 — the X stream needs the
+    // deeper buffer, so X and W1 have separate rings (XS x 16 KB, WS x 32 KB per CTA).
     const XPlan xp = xplan_make(off, n, m0, lane);
-    const uint32_t lead_full0 = mapa(full0, 0u);
-    const int pre = kblocks < WSTAGES ? kblocks : WSTAGES;
-    // W1 tiles of the first stages do not depend on an earlier kernel (PDL overlap)
-    if (lane == 0)
-      for (int i = 0; i < pre; ++i) {
-        if (r == 0) mbar_expect_tx(full0 + 8 * i, 2 * WSTAGE);
-        const uint32_t sb = s0 + i * WSTAGE + WA;
-        tma_load_2d_pair(sb, &tmap_w, lead_full0 + 8 * i, i * WBK, (int)r * 128);
-        tma_load_2d_pair(sb + WBH, &tmap_w, lead_full0 + 8 * i, i * WBK, 256 + (int)r * 128);
-      }
+    const uint32_t lead_xfull0 = mapa(xfull0, 0u);
+    const uint32_t x_tx = skip_x ? 0u : (uint32_t)(2 * WA);
     if (xp.tile_xs) {
       // decode/prefill split: this launch was promised decode-only tiles (trail_set_prefill_start)
       if (decode_only) {
@@ -138,47 +149,62 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
     }
     __syncwarp();
     for (int i = 0; i < kblocks; ++i) {
-      const int st = i % WSTAGES;
-      const int kc = i * WBK;
-      if (i >= WSTAGES) {
-        if (lane == 0) {
-          mbar_wait(empty0 + 8 * st, ((uint32_t)(i / WSTAGES) & 1u) ^ 1u);
-          if (r == 0) mbar_expect_tx(full0 + 8 * st, 2 * WSTAGE);
-          const uint32_t sb = s0 + st * WSTAGE + WA;
-          tma_load_2d_pair(sb, &tmap_w, lead_full0 + 8 * st, kc, (int)r * 128);
-          tma_load_2d_pair(sb + WBH, &tmap_w, lead_full0 + 8 * st, kc, 256 + (int)r * 128);
-        }
-        __syncwarp();
+      const int st = i % XS;
+      if (lane == 0) {
+        if (i >= XS) mbar_wait(xempty0 + 8 * st, ((uint32_t)(i / XS) & 1u) ^ 1u);
+        if (r == 0) mbar_expect_tx(xfull0 + 8 * st, x_tx);
       }
-      xplan_issue<true>(xp, lane, s0 + st * WSTAGE, lead_full0 + 8 * st, kc, &tmap_emb, &tmap_emb4,
-                        &tmap_emb32, &tmap_xs, &tmap_xs4, &tmap_xs32);
+      __syncwarp();
+      if (!skip_x)
+        xplan_issue<true>(xp, lane, s0 + st * WA, lead_xfull0 + 8 * st, i * WBK, &tmap_emb,
+                          &tmap_emb4, &tmap_emb32, &tmap_xs, &tmap_xs4, &tmap_xs32);
     }
+  } else if (warp == 2) {
+    // ---- W1 producer (lane 0): my halves of the two N = 256 column blocks into the W1 ring;
+    // W1 does not depend on an earlier kernel, so the first stages overlap its tail (PDL)
+    if (lane == 0) {
+      const uint32_t lead_wfull0 = mapa(wfull0, 0u);
+      const uint32_t w_tx = skip_w ? 0u : (uint32_t)(4 * WBH);
+      for (int i = 0; i < kblocks; ++i) {
+        const int st = i % WS;
+        if (i >= WS) mbar_wait(wempty0 + 8 * st, ((uint32_t)(i / WS) & 1u) ^ 1u);
+        if (r == 0) mbar_expect_tx(wfull0 + 8 * st, w_tx);
+        const uint32_t sb = s0 + XS * WA + st * 2 * WBH;
+        if (!skip_w) {
+          tma_load_2d_pair(sb, &tmap_w, lead_wfull0 + 8 * st, i * WBK, (int)r * 128);
+          tma_load_2d_pair(sb + WBH, &tmap_w, lead_wfull0 + 8 * st, i * WBK, 256 + (int)r * 128);
+        }
+      }
+    }
+    __syncwarp();
   } else if (warp == 1) {
     if (lane == 0 && r == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(2 * WBM, 256);
       for (int i = 0; i < kblocks; ++i) {
-        const int st = i % WSTAGES;
-        mbar_wait(full0 + 8 * st, (uint32_t)(i / WSTAGES) & 1u);
+        const int sx = i % XS, sw = i % WS;
+        mbar_wait(xfull0 + 8 * sx, (uint32_t)(i / XS) & 1u);
+        mbar_wait(wfull0 + 8 * sw, (uint32_t)(i / WS) & 1u);
         tc_fence_after();
-        const uint32_t sa = s0 + st * WSTAGE;
-        const uint64_t da = sw128_kmajor_desc(sa);
+        const uint64_t da = sw128_kmajor_desc(s0 + sx * WA);
+        const uint32_t sb = s0 + XS * WA + sw * 2 * WBH;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const uint64_t db = sw128_kmajor_desc(sa + WA + h * WBH);
+          const uint64_t db = sw128_kmajor_desc(sb + h * WBH);
 #pragma unroll
           for (int kk = 0; kk < WBK / 16; ++kk)
             umma_bf16_pair(tmem + 256 * h, da + 2 * kk, db + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit_pair(empty0 + 8 * st);
+        umma_commit_pair(xempty0 + 8 * sx);
+        umma_commit_pair(wempty0 + 8 * sw);
       }
       umma_commit_pair(done);
     }
     __syncwarp();
   } else {
-    // b1, head constants and this CTA's slot state (weights and state written by kernels that
-    // completed before the pool kernel passed its own griddep_wait: PDL chain)
-    const int t = tid - 64;
-    for (int v = t; v < WH / 4; v += WT - 64)
+    // warps 3-7: b1, head constants and this CTA's slot state (weights and state written by
+    // kernels that completed before the pool kernel passed its own griddep_wait: PDL chain)
+    const int t = tid - 96;
+    for (int v = t; v < WH / 4; v += WT - 96)
       reinterpret_cast<float4 *>(b1s)[v] = __ldg(reinterpret_cast<const float4 *>(b1) + v);
     if (t < kMaxBins) {
       hs.m[t] = cst.m[t];
@@ -285,6 +311,16 @@ int wide_min_n() {
   return v;
 }
 
+// TRAIL_WIDE_DIAG: 1 = skip the X loads, 2 = skip the W1 loads, 3 = both (timing probes of
+// the MMA / load paths, scripts/wide_probe.py — wrong results)
+static int wide_flags() {
+  static const int v = [] {
+    const char *g = getenv("TRAIL_WIDE_DIAG");
+    return (g ? atoi(g) & 3 : 0) << 8;
+  }();
+  return v;
+}
+
 template <int KB>
 static cudaError_t wide_attr() {
   return cudaFuncSetAttribute(trail_wide_predict_kernel<KB>,
@@ -332,7 +368,8 @@ cudaError_t launch_wide_predict(Ctx &c, const void *emb, int64_t ld, const int32
                             c.tmap_emb32, c.tmap_xs1, c.tmap_xs4, c.tmap_xs32, c.tmap_w128, off, \
                             n, c.d / WBK, (const float *)c.b1, (const float *)c.w2,              \
                             (const float *)c.b2, c.host_consts, ids, is_prefill, prior_override, \
-                            c.cfg.max_slots, c.lq, c.meta, post, L, c.dev_err, decode_only)
+                            c.cfg.max_slots, c.lq, c.meta, post, L, c.dev_err, decode_only,     \
+                            wide_flags())
   switch (wide_kb(c.k)) {
     case 10: TRAIL_WIDE(10);
     case 16: TRAIL_WIDE(16);
