@@ -14,12 +14,14 @@
 // and an O(b^2) in-bucket ranking (measured: 49 us of a 65 us selection at configs[3] with
 // L buckets; 4.7 ms for an 81 920-record unseen burst).
 //   B0  1024 samples of (composite key, input position) on a jittered stride are ranked by
-//       counting (a warp per sample over the staged sample set); sample of rank r becomes
+//       counting (32 samples per CTA, one per lane, each warp against a 32-key slice of the
+//       staged sample set, partial counts summed in shared memory); sample of rank r becomes
 //       splitter r - 1, so the 1023 splitters cut the records into 1024 buckets of about
 //       m / 1024 whatever the key distribution (a tie cluster is split by arrival like any
 //       other run of keys).  On the local path B0 also builds every record (row a4).
 //   B1  bucket of each record = binary search over the splitters (shared memory); histogram
-//       of (count, KV, running) per bucket + forced totals (warp-aggregated global atomics)
+//       of (count, KV, running) per bucket in shared memory, added to the global histogram
+//       one bucket per thread; forced totals
 //   B2  scatter of the records into bucket order (prefix of the counts, atomic cursors; the
 //       bucket ids B1 found are reused)
 //   B3  each record counts the records of its own bucket ordered before it (the bucket range
@@ -29,6 +31,7 @@
 // Cost is O(m log m + sum over buckets of size^2 / 8) with bucket sizes ~ m / 1024.
 #include <algorithm>
 
+#include "sm100_ptx.cuh"
 #include "trail_internal.cuh"
 
 namespace trail {
@@ -37,10 +40,13 @@ namespace {
 constexpr int kB = 1024;                // buckets (= samples: every sample but the smallest
 constexpr int kS = kB;                  //  is a splitter)
 constexpr int kB0Threads = 1024;
+constexpr int kB1Threads = 1024;
 constexpr int kB3Threads = 1024;
 constexpr int kB3Tpi = 8;               // threads per record in B3
 constexpr int kB3Items = kB3Threads / kB3Tpi;
 constexpr int kStageCap = 4096;         // bucket entries staged in shared memory (64 KB)
+// per-CTA phase traces (trail_trace_*, diagnostics): trace rows of B3, B0, B1, B2
+constexpr int kTrB3 = 2048, kTrB0 = 3072, kTrB1 = 3136, kTrB2 = 3584;
 
 struct BkEntry {                        // bucket-sorted record (16 B)
   unsigned long long key;               // keybits << 32 | arrival
@@ -151,11 +157,14 @@ trail_bucket_sample_kernel(const Record *__restrict__ rec, Record *__restrict__ 
                            const int32_t *__restrict__ kvin, const uint8_t *__restrict__ running,
                            const SlotMeta *__restrict__ meta, const HeadConsts *__restrict__ cst,
                            int max_slots, uint32_t id_base, uint32_t *__restrict__ err, int m,
-                           BkKey *__restrict__ spl) {
+                           BkKey *__restrict__ spl, uint64_t *__restrict__ trace) {
   __shared__ BkKey smp[kS];                                   // 32 KB
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  uint64_t *tr = trace ? trace + 16 * (kTrB0 + (int64_t)blockIdx.x) : nullptr;   // diagnostics
+  if (tr && t == 0) tr[0] = ptx::gtimer();
   griddep_wait();     // records from the pack kernel / the all-gather, or the slot state
   griddep_launch();
+  if (tr && t == 0) tr[1] = ptx::gtimer();
   // local path: every record, grid-stride (row a4, the record build of trail_schedule_pack)
   if (!rec)
     for (int i = blockIdx.x * kB0Threads + t; i < m; i += gridDim.x * kB0Threads)
@@ -182,56 +191,69 @@ trail_bucket_sample_kernel(const Record *__restrict__ rec, Record *__restrict__ 
     smp[j] = k;
   }
   __syncthreads();
-  // one warp per sample: its rank r among the samples; rank r >= 1 is splitter r - 1
-  for (int j = blockIdx.x * (kB0Threads / 32) + warp; j < kS; j += gridDim.x * (kB0Threads / 32)) {
-    const BkKey me = smp[j];
+  if (tr && t == 0) tr[2] = ptx::gtimer();
+  // ranks of this CTA's 32 samples (lane l of every warp: sample 32c + l) by counting, warp w
+  // against the key slice [32w, 32w + 32) (broadcast reads), partial counts added in shared
+  // memory; rank r >= 1 makes the sample splitter r - 1
+  __shared__ uint32_t s_rank[32];
+  if (t < 32) s_rank[t] = 0u;
+  __syncthreads();
+  for (int j0 = blockIdx.x * 32; j0 < kS; j0 += gridDim.x * 32) {
+    const BkKey me = smp[j0 + lane];
     uint32_t cnt = 0;
-#pragma unroll 4
-    for (int q = lane; q < kS; q += 32) {
+#pragma unroll 8
+    for (int q = 32 * warp; q < 32 * warp + 32; ++q) {
       const BkKey o = smp[q];
       cnt += bk_lt(o.key, o.idx, me.key, me.idx) ? 1u : 0u;
     }
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if (lane == 0 && cnt > 0) spl[cnt - 1] = me;
+    atomicAdd(&s_rank[lane], cnt);
+    __syncthreads();
+    if (t < 32) {
+      const uint32_t r = s_rank[t];
+      if (r > 0) spl[r - 1] = smp[j0 + t];
+      s_rank[t] = 0u;
+    }
+    __syncthreads();
   }
+  if (tr && t == 0) tr[3] = ptx::gtimer();
 }
 
-// B1: per-bucket totals (+ forced count / KV)
-__global__ void __launch_bounds__(256)
+// B1: per-bucket totals (+ forced count / KV): a shared-memory histogram per CTA, added to the
+// global one bucket per thread (the warp-aggregated global atomics it replaces serialised on
+// match_any groups: 8 us at configs[3])
+__global__ void __launch_bounds__(kB1Threads)
 trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, const BkKey *__restrict__ spl_g,
                          uint32_t *__restrict__ hcnt, uint32_t *__restrict__ hrun,
                          unsigned long long *__restrict__ hkv,
                          unsigned long long *__restrict__ forced_tot,
-                         uint16_t *__restrict__ bkid) {
+                         uint16_t *__restrict__ bkid, uint64_t *__restrict__ trace) {
   __shared__ BkKey spl[kB];
+  __shared__ uint32_t h_cnt[kB], h_run[kB];
+  __shared__ unsigned long long h_kv[kB];
+  uint64_t *tr = trace ? trace + 16 * (kTrB1 + (int64_t)blockIdx.x) : nullptr;   // diagnostics
+  if (tr && threadIdx.x == 0) tr[0] = ptx::gtimer();
+  for (int q = threadIdx.x; q < kB; q += kB1Threads) { h_cnt[q] = 0u; h_run[q] = 0u; h_kv[q] = 0ull; }
   griddep_wait();     // splitters (and local records) from B0
   griddep_launch();
-  for (int q = threadIdx.x; q < kB - 1; q += blockDim.x) spl[q] = spl_g[q];
+  if (tr && threadIdx.x == 0) tr[1] = ptx::gtimer();
+  for (int q = threadIdx.x; q < kB - 1; q += kB1Threads) spl[q] = spl_g[q];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  for (int i0 = blockIdx.x * blockDim.x; i0 < m; i0 += gridDim.x * blockDim.x) {
+  for (int i0 = blockIdx.x * kB1Threads; i0 < m; i0 += gridDim.x * kB1Threads) {
     const int i = i0 + threadIdx.x;
-    int b = -1;
-    uint32_t kvv = 0, runn = 0, frc = 0;
+    uint32_t kvv = 0, frc = 0;
     if (i < m) {
       const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(rec + i));
+      int b = -1;
       if (v.x != kPadKey) {
         b = bk_bucket(spl, rec_key(v.x, v.y), (uint32_t)i);
         kvv = v.z;
-        runn = v.w >> 31;
         frc = (v.x >> 31) == 0u ? 1u : 0u;
+        atomicAdd(&h_cnt[b], 1u);
+        if (v.w >> 31) atomicAdd(&h_run[b], 1u);
+        atomicAdd(&h_kv[b], (unsigned long long)kvv);
       }
       bkid[i] = (uint16_t)(b < 0 ? 0xFFFF : b);   // reused by B2 (no second search)
-    }
-    const unsigned peers = __match_any_sync(0xffffffffu, b);
-    const uint32_t c = __popc(peers);
-    const uint32_t r = __reduce_add_sync(peers, runn);
-    const uint32_t klo = __reduce_add_sync(peers, kvv & 0xFFFFu);
-    const uint32_t khi = __reduce_add_sync(peers, kvv >> 16);
-    if (b >= 0 && lane == __ffs(peers) - 1) {
-      atomicAdd(hcnt + b, c);
-      if (r) atomicAdd(hrun + b, r);
-      atomicAdd(hkv + b, ((unsigned long long)khi << 16) + klo);
     }
     // forced totals: count in the high 24 bits, KV in the low 40 (both far below the caps)
     const uint32_t fc = __reduce_add_sync(0xffffffffu, frc);
@@ -240,6 +262,14 @@ trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, const BkKey *__r
     if (lane == 0 && fc)
       atomicAdd(forced_tot, ((unsigned long long)fc << 40) + ((unsigned long long)fhi << 16) + flo);
   }
+  __syncthreads();
+  for (int q = threadIdx.x; q < kB; q += kB1Threads)
+    if (h_cnt[q]) {
+      atomicAdd(hcnt + q, h_cnt[q]);
+      if (h_run[q]) atomicAdd(hrun + q, h_run[q]);
+      atomicAdd(hkv + q, h_kv[q]);
+    }
+  if (tr && threadIdx.x == 0) tr[2] = ptx::gtimer();
 }
 
 // B2: scatter into bucket order
@@ -248,12 +278,17 @@ trail_bucket_scatter_kernel(const Record *__restrict__ rec, int m,
                             const uint16_t *__restrict__ bkid,
                             const uint32_t *__restrict__ hcnt, const uint32_t *__restrict__ hrun,
                             const unsigned long long *__restrict__ hkv,
-                            uint32_t *__restrict__ cursor, BkEntry *__restrict__ sorted) {
+                            uint32_t *__restrict__ cursor, BkEntry *__restrict__ sorted,
+                            uint64_t *__restrict__ trace) {
   extern __shared__ __align__(16) uint8_t bsm[];
   BkScan &sh = *reinterpret_cast<BkScan *>(bsm);
+  uint64_t *tr = trace ? trace + 16 * (kTrB2 + (int64_t)blockIdx.x) : nullptr;   // diagnostics
+  if (tr && threadIdx.x == 0) tr[0] = ptx::gtimer();
   griddep_wait();
   griddep_launch();
+  if (tr && threadIdx.x == 0) tr[1] = ptx::gtimer();
   bk_scan_buckets(sh, hcnt, hrun, hkv);       // (synchronises)
+  if (tr && threadIdx.x == 0) tr[2] = ptx::gtimer();
   const int lane = threadIdx.x & 31;
   for (int i0 = blockIdx.x * blockDim.x; i0 < m; i0 += gridDim.x * blockDim.x) {
     const int i = i0 + threadIdx.x;
@@ -278,6 +313,7 @@ trail_bucket_scatter_kernel(const Record *__restrict__ rec, int m,
       sorted[slot] = e;
     }
   }
+  if (tr && threadIdx.x == 0) tr[3] = ptx::gtimer();
 }
 
 // B3: exact positions, cumulative KV, running-before; lists
@@ -289,17 +325,21 @@ trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, uint32_t *__rest
                          long long budget, int max_run, unsigned long long *__restrict__ gcnt,
                          uint2 *__restrict__ scratch, uint32_t *__restrict__ run_ids,
                          uint32_t *__restrict__ pre_ids, uint32_t *__restrict__ adm_ids,
-                         int32_t *__restrict__ counts) {
+                         int32_t *__restrict__ counts, uint64_t *__restrict__ trace) {
   extern __shared__ __align__(16) uint8_t bsm[];
   BkScan &sh = *reinterpret_cast<BkScan *>(bsm);
   BkEntry *stage = reinterpret_cast<BkEntry *>(bsm + sizeof(BkScan));
   __shared__ int s_lo, s_hi, s_last;
   __shared__ uint32_t s_run, s_rcut;
   __shared__ unsigned long long s_tot;
+  uint64_t *tr = trace ? trace + 16 * (kTrB3 + (int64_t)blockIdx.x) : nullptr;   // diagnostics
+  if (tr && threadIdx.x == 0) tr[0] = ptx::gtimer();
   griddep_wait();
   griddep_launch();
   const int t = threadIdx.x;
+  if (tr && t == 0) tr[1] = ptx::gtimer();
   bk_scan_buckets(sh, hcnt, hrun, hkv);
+  if (tr && t == 0) tr[2] = ptx::gtimer();
   const int nv = (int)(sh.cnt[kB - 1] + __ldcg(hcnt + kB - 1));
   const unsigned long long ft = __ldcg(forced_tot);
   const int nf = (int)(ft >> 40);
@@ -331,6 +371,7 @@ trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, uint32_t *__rest
   if (staged)
     for (int q = lo + t; q < hi; q += kB3Threads) stage[q - lo] = sorted[q];
   __syncthreads();
+  if (tr && t == 0) tr[3] = ptx::gtimer();
   // kB3Tpi threads per record
   const int li = t / kB3Tpi, part = t % kB3Tpi;
   const int p = p0 + li;
@@ -377,6 +418,7 @@ trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, uint32_t *__rest
     scratch[pos] = make_uint2(gidw, rbefore);
   }
   __syncthreads();
+  if (tr && t == 0) tr[4] = ptx::gtimer();
   if (t == 0) {
     const unsigned long long inc = (1ull << 48) | ((unsigned long long)s_run << 24) | s_rcut;
     unsigned long long old;
@@ -387,12 +429,22 @@ trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, uint32_t *__rest
     s_tot = tot;
   }
   __syncthreads();
+  if (tr && t == 0) { tr[5] = ptx::gtimer(); tr[14] = (uint64_t)s_last; }
   if (!s_last) return;
   const int n_run = (int)((s_tot >> 24) & 0xFFFFFFull);
   const int R_cut = (int)(s_tot & 0xFFFFFFull);
-  for (int q = n_run + t; q < nv; q += kB3Threads) {
-    const uint2 v = __ldcg(scratch + q);
-    if (v.x >> 31) pre_ids[(int)v.y - R_cut] = v.x & 0x7FFFFFFFu;
+  // positions past the cut: 8 independent loads per thread in flight per round (a plain
+  // load -> store loop is one L2 round trip per 1024 records)
+  for (int q0 = n_run; q0 < nv; q0 += 8 * kB3Threads) {
+    uint2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = q0 + u * kB3Threads + t;
+      v[u] = q < nv ? __ldcg(scratch + q) : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (v[u].x >> 31) pre_ids[(int)v[u].y - R_cut] = v[u].x & 0x7FFFFFFFu;
   }
   // re-arm the histogram and cursors for the next call (every CTA has finished with them)
   for (int q = t; q < kB; q += kB3Threads) { hcnt[q] = 0u; hrun[q] = 0u; hkv[q] = 0ull; cursor[q] = 0u; }
@@ -403,6 +455,7 @@ trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, uint32_t *__rest
     counts[2] = n_run - R_cut;
     counts[3] = over ? TRAIL_WARN_OVER_BUDGET : TRAIL_OK;
   }
+  if (tr && t == 0) tr[6] = ptx::gtimer();
 }
 
 // ------------------------------------------------------------------ host
@@ -439,27 +492,29 @@ cudaError_t launch_select_bucket(const Ctx &c, const Record *rec_in, Record *rec
   uint2 *scratch = reinterpret_cast<uint2 *>(sorted + c.bk_cap);
   uint16_t *bkid = reinterpret_cast<uint16_t *>(scratch + c.bk_cap);
   // B0: enough CTAs to build the records (local path) and a warp per sample
-  const int g0 = std::max(kS / (kB0Threads / 32),
-                          rec_in ? 0 : std::min(c.num_sms, (m + kB0Threads - 1) / kB0Threads));
+  const int g0 = std::max(kS / 32, rec_in ? 0 : std::min(c.num_sms, (m + kB0Threads - 1) / kB0Threads));
   cudaError_t e = launch_k(trail_bucket_sample_kernel, dim3(g0), dim3(kB0Threads), 0, s, rec_in,
                            rec_out, ids, arrival, kv, running, (const SlotMeta *)c.meta,
                            (const HeadConsts *)c.consts, c.cfg.max_slots, c.cfg.id_base,
-                           c.dev_err, m, spl);
+                           c.dev_err, m, spl, (c.trace && kTrB0 + g0 <= c.trace_cap) ? c.trace : nullptr);
   if (e != cudaSuccess) return e;
-  const int g1 = std::max(1, std::min(2 * c.num_sms, (m + 255) / 256));
-  e = launch_k(trail_bucket_hist_kernel, dim3(g1), dim3(256), 0, s, rec, m, (const BkKey *)spl,
-               hcnt, hrun, hkv, forced_tot, bkid);
+  const int g1 = std::max(1, std::min(c.num_sms, (m + kB1Threads - 1) / kB1Threads));
+  e = launch_k(trail_bucket_hist_kernel, dim3(g1), dim3(kB1Threads), 0, s, rec, m, (const BkKey *)spl,
+               hcnt, hrun, hkv, forced_tot, bkid,
+               (c.trace && kTrB1 + g1 <= c.trace_cap && g1 <= kTrB2 - kTrB1) ? c.trace : nullptr);
   if (e != cudaSuccess) return e;
   const int g2 = std::max(1, std::min(c.num_sms, (m + kB3Threads - 1) / kB3Threads));
   e = launch_k(trail_bucket_scatter_kernel, dim3(g2), dim3(kB3Threads), sizeof(BkScan), s, rec, m,
                (const uint16_t *)bkid, (const uint32_t *)hcnt, (const uint32_t *)hrun,
-               (const unsigned long long *)hkv, cursor, sorted);
+               (const unsigned long long *)hkv, cursor, sorted,
+               (c.trace && kTrB2 + g2 <= c.trace_cap) ? c.trace : nullptr);
   if (e != cudaSuccess) return e;
   const int g3 = std::max(1, (m + kB3Items - 1) / kB3Items);
   return launch_k(trail_bucket_rank_kernel, dim3(g3), dim3(kB3Threads),
                   sizeof(BkScan) + kStageCap * sizeof(BkEntry), s, rec, m, hcnt, hrun, hkv,
                   forced_tot, cursor, (const BkEntry *)sorted, (long long)budget, max_run, gcnt,
-                  scratch, run, pre, adm, counts);
+                  scratch, run, pre, adm, counts,
+                  (c.trace && g3 <= kTrB0 - kTrB3) ? c.trace : nullptr);
 }
 
 }  // namespace trail

@@ -35,7 +35,7 @@ namespace trail {
 
 namespace {
 constexpr int kT = 512;               // threads per CTA
-constexpr int kRankCap = 8192;        // keys staged in shared memory (64 KB)
+constexpr int kRankCap = kRankMaxRecords;   // records staged in shared memory (32 KB)
 
 struct RkShared {
   long long v0[kT / 32], v1[kT / 32];
@@ -141,10 +141,30 @@ trail_select_rank_kernel(const Record *__restrict__ rec_in, Record *__restrict__
   // 1. every record's key, kv and flags -> shared memory; forced count / KV, running count
   long long fkv_t = 0;
   int f_t = 0, r_t = 0, v_t = 0;
-  for (int j = tid; j < n; j += kT) {
+  // every dependent load of a thread (slot state / given records) issued before any is used:
+  // one L2 round trip after the wait instead of one per 512 records
+  constexpr int kPer = kRankCap / kT;
+  SlotMeta mt[kPer];
+  Record rin[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int j = tid + u * kT;
+    if (j < n) {
+      if (rec_in) {
+        rin[u] = rec_in[j];
+      } else {
+        const uint32_t slot = sitem[j].gid & 0x7FFFFFFFu;
+        if (slot < (uint32_t)max_slots) mt[u] = meta[slot];
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int j = tid + u * kT;
+    if (j >= n) break;
     Record r;
     if (rec_in) {
-      r = rec_in[j];
+      r = rin[u];
     } else {   // row a4 from the staged inputs + the slot state
       const RkItem in = sitem[j];
       const uint32_t slot = in.gid & 0x7FFFFFFFu;
@@ -157,7 +177,7 @@ trail_select_rank_kernel(const Record *__restrict__ rec_in, Record *__restrict__
       float key = cst->prior_L;
       bool forced = false;
       if (slot < (uint32_t)max_slots) {
-        const SlotMeta m = meta[slot];
+        const SlotMeta m = mt[u];
         if (m.flags & 1u) {
           key = m.L;
           forced = run && (m.age >= m.thr);
@@ -287,9 +307,17 @@ trail_select_rank_kernel(const Record *__restrict__ rec_in, Record *__restrict__
   const int n_run = (int)((s_tot >> 24) & 0xFFFFFFull);
   const int R_cut = (int)(s_tot & 0xFFFFFFull);
   if (tr && tid == 0) tr[5] = ptx::gtimer();
-  for (int p = n_run + tid; p < nv; p += kT) {
-    const uint2 v = __ldcg(scratch + p);
-    if (v.x >> 31) pre_ids[(int)v.y - R_cut] = v.x & 0x7FFFFFFFu;
+  // positions past the cut: all loads of a thread in flight before its stores
+  for (int p0 = n_run; p0 < nv; p0 += 4 * kT) {
+    uint2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = p0 + u * kT + tid;
+      v[u] = p < nv ? __ldcg(scratch + p) : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v[u].x >> 31) pre_ids[(int)v[u].y - R_cut] = v[u].x & 0x7FFFFFFFu;
   }
   if (tr && tid == 0) tr[6] = ptx::gtimer();
   __syncthreads();
@@ -304,8 +332,6 @@ trail_select_rank_kernel(const Record *__restrict__ rec_in, Record *__restrict__
 }
 
 // ------------------------------------------------------------------ host
-int select_rank_capacity() { return kRankCap; }
-
 cudaError_t select_rank_prepare() {
   cudaError_t e = cudaFuncSetAttribute(trail_select_rank_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
