@@ -51,6 +51,9 @@ CONFIGS = {
                desc="16384 requests/GPU at d=8192 (70B-shaped), 20 bins, tcgen05 GEMM regime"),
 }
 
+L1_NAMES = {1: "gemv", 2: "tcgen05 split-K (K2c)", 3: "tcgen05 unfused",
+            4: "tcgen05 CTA pair (K2d)", 5: "3xTF32 tcgen05 (K2t)"}
+
 
 def sm_max_mhz():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -405,7 +408,19 @@ def measure(args, cfg_name, rank, world, local, device, main):
         # lanes x 2 flop x SM clock; its ridge is ~11 flop/B
         alu_tf = torch.cuda.get_device_properties(device).multi_processor_count * 128 * 2 * \
             sm_max_mhz() * 1e6 / 1e12
-        if dom == "gemv" and ach_tf / alu_tf > ach_bw / hbm:
+        # 3xTF32 on the tensor cores (K2t, fp32 handles): tf32 runs at half the bf16 rate
+        # (nominal ratio) and every algorithmic product costs 3 MMAs
+        tf32_eff = tf_sust / 2.0 / 3.0
+        if dom == "gemv" and mode == 5:
+            if ach_tf / tf32_eff > ach_bw / hbm:
+                roof = {"bound": "tensor", "achieved": ach_tf, "peak": tf32_eff, "unit": "TFLOP/s",
+                        "frac": ach_tf / tf32_eff,
+                        "peak_note": "3xTF32: sustained bf16 peak x 1/2 (tf32 nominal ratio) / 3 "
+                                     "MMAs per product"}
+            else:
+                roof = {"bound": "hbm", "achieved": ach_bw, "peak": hbm, "unit": "GB/s",
+                        "frac": ach_bw / hbm}
+        elif dom == "gemv" and ach_tf / alu_tf > ach_bw / hbm:
             roof = {"bound": "alu", "achieved": ach_tf, "peak": alu_tf, "unit": "TFLOP/s",
                     "frac": ach_tf / alu_tf,
                     "peak_note": "fp32 FFMA: SMs x 128 lanes x 2 flop x max SM clock"}
@@ -505,7 +520,7 @@ def measure(args, cfg_name, rank, world, local, device, main):
                 "workload": workload_name(cfg_name, world),
                 "n_total": cfg["n"] * world, "n_per_gpu": cfg["n"], "waiting_per_gpu": cfg["waiting"], "d": cfg["d"],
                 "hidden": cfg["H"], "bins": cfg["k"], "c": cfg["c"],
-                "l1_kernel": {1: "gemv", 2: "tcgen05 split-K (K2c)", 3: "tcgen05 unfused", 4: "tcgen05 CTA pair (K2d)"}[mode], "l1_splits": splits,
+                "l1_kernel": L1_NAMES[mode], "l1_splits": splits,
                 "l2": "flushed between timed steps, outside the step events: a 256 MiB memset "
                       "(> the 126 MB L2) then a 256 MiB read of another buffer, so the step "
                       "starts with none of its data in L2 and no dirty lines to write back"
@@ -607,7 +622,7 @@ def run_sweep(args):
             trail_profile_enable(t.h, 0)
             kus = {kn: 1e3 * statistics.median(v) for kn, v in kern.items()}
             mode, splits = trail_plan_l1(t.h, int(bs[1].n))
-            l1 = "gemv" if mode == 1 else "umma"
+            l1 = "gemv" if mode in (1, 5) else "umma"
             l1_us = kus.get(l1)
             byts = 512 * d * 2 + bs[1].n * d * 2
             flops = 2.0 * bs[1].n * d * 512
@@ -617,8 +632,7 @@ def run_sweep(args):
                    "us_per_step_p99": 1e3 * st_[min(len(st_) - 1, int(math.ceil(0.99 * len(st_))) - 1)],
                    "requests_per_s": n / (statistics.median(ms) / 1e3),
                    "kernel_us": {kk: round(v, 3) for kk, v in kus.items()},
-                   "l1_kernel": {1: "gemv", 2: "tcgen05 split-K (K2c)", 3: "tcgen05 unfused",
-                                 4: "tcgen05 CTA pair (K2d)"}[mode],
+                   "l1_kernel": L1_NAMES[mode],
                    "l1_bytes": byts, "l1_flops": flops,
                    "l1_hbm_frac": (byts / (l1_us / 1e6) / 1e9 / hbm) if l1_us else None,
                    "l1_tensor_frac_burst": (flops / (l1_us / 1e6) / 1e12 / tf_burst) if l1_us else None}

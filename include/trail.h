@@ -60,9 +60,13 @@ typedef enum {
                           layer 2 and head in the epilogue (bf16 only) */
   TRAIL_L1_UMMA_UNFUSED = 3, /* K2b + K3: tcgen05 layer 1 with split-K partials in global
                                 memory, then the separate head kernel (bf16 only) */
-  TRAIL_L1_WIDE = 4    /* K2d: CTA-pair (cta_group::2) tcgen05 layer 1 over the whole hidden
+  TRAIL_L1_WIDE = 4,   /* K2d: CTA-pair (cta_group::2) tcgen05 layer 1 over the whole hidden
                           width (H = 512) in TMEM, layer 2 and head in the epilogue; AUTO picks
                           it for large n (bf16, H = 512 only) */
+  TRAIL_L1_TF32 = 5    /* K2t + K3: fp32 handles — tcgen05 kind::tf32 layer 1 with an exact
+                          hi/lo operand split (3 MMAs per product, fp32-level accuracy), split-K
+                          partials, then the head kernel (fp32 only; H % 128 == 0, d % 4 == 0;
+                          AUTO keeps K2a) */
 } trail_l1_mode;
 
 /* Sticky device-side error bits (trail_device_errors). */

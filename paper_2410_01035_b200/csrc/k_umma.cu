@@ -185,6 +185,21 @@ bool encode_rows_bf16(CUtensorMap *m, const void *base, uint64_t cols, uint64_t 
   return r == CUDA_SUCCESS;
 }
 
+// fp32 row-major [rows][ld] (cols used), SWIZZLE_128B boxes of box_cols (<= 32) x box_rows (K2t)
+bool encode_rows_f32_sw128(CUtensorMap *m, const void *base, uint64_t cols, uint64_t rows,
+                           uint64_t ld, uint32_t box_cols, uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // plain (no swizzle) 2-D map of a row-major [rows][ld] fp32/bf16 matrix, boxes box_cols x box_rows
 bool encode_plain_2d(CUtensorMap *m, const void *base, bool bf16, uint64_t cols, uint64_t rows,
                      uint64_t ld, uint32_t box_cols, uint32_t box_rows) {

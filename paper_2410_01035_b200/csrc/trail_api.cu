@@ -63,9 +63,26 @@ struct ProfScope {
   }
 };
 
-void plan_l1(const Ctx &c, int n, int *mode, int *bn, int *splits) {
+void plan_l1(const Ctx &c, int n, int *mode, int *bn, int *splits, bool planning = false) {
   int m = c.cfg.l1_mode;
-  if (c.dtype == TRAIL_F32) m = TRAIL_L1_GEMV;
+  if (c.dtype == TRAIL_F32) {
+    // fp32: the 3xTF32 tensor-core layer 1 (K2t) unless the CUDA-core GEMV is forced
+    // AUTO keeps the CUDA-core GEMV K2a: measured at configs[0], K2t's launch is shorter
+    // (14.4 vs 18.2 us) but the step is longer (median 38.9 vs 32.8 us);
+    // TRAIL_FP32_L1=tf32 makes AUTO pick K2t (A/B runs)
+    static const bool tf32_env = [] {
+      const char *e = getenv("TRAIL_FP32_L1");
+      return e && e[0] == 't';
+    }();
+    const bool tf32_ok = tf32_supported(c) || (planning && c.H % 128 == 0 && c.d % 4 == 0);
+    if ((m == TRAIL_L1_TF32 || (m == TRAIL_L1_AUTO && tf32_env)) && tf32_ok) {
+      *mode = TRAIL_L1_TF32;
+      *bn = 0;
+      *splits = tf32_splits(c);
+      return;
+    }
+    m = TRAIL_L1_GEMV;
+  }
   else if (m == TRAIL_L1_AUTO) m = (n <= kGemvMaxN) ? TRAIL_L1_GEMV : TRAIL_L1_UMMA;
   if (m == TRAIL_L1_UMMA && c.cfg.l1_mode == TRAIL_L1_AUTO && wide_supported(c) && n >= wide_min_n())
     m = TRAIL_L1_WIDE;
@@ -173,11 +190,12 @@ size_t partial_elems_needed(const Ctx &c) {
     for (int forced = 0; forced < 2; ++forced) {
       Ctx tmp_c;
       tmp_c.cfg = c.cfg;
-      tmp_c.cfg.l1_mode = forced ? TRAIL_L1_GEMV : TRAIL_L1_UMMA_UNFUSED;
-      if (c.dtype == TRAIL_F32 && !forced) continue;
+      // bf16: the GEMV and unfused tcgen05 plans; fp32: the GEMV and 3xTF32 plans
+      tmp_c.cfg.l1_mode = forced ? TRAIL_L1_GEMV
+                                 : (c.dtype == TRAIL_F32 ? TRAIL_L1_AUTO : TRAIL_L1_UMMA_UNFUSED);
       tmp_c.d = c.d; tmp_c.H = c.H; tmp_c.dtype = c.dtype; tmp_c.num_sms = c.num_sms;
       int mode, bn, s;
-      plan_l1(tmp_c, n, &mode, &bn, &s);
+      plan_l1(tmp_c, n, &mode, &bn, &s, true);
       best = std::max(best, (size_t)s * (size_t)n * (size_t)c.H);
     }
   }
@@ -219,8 +237,10 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
   if (g.max_slots <= 0 || g.max_requests <= 0 || g.max_sched < 0) return TRAIL_ERR_INVALID;
   if (g.max_requests > (1 << 18)) return TRAIL_ERR_INVALID;   // K1 offset search bound
   if (g.world_size < 1) return TRAIL_ERR_INVALID;
-  if (g.l1_mode < 0 || g.l1_mode > 4) return TRAIL_ERR_INVALID;
-  if (g.l1_mode >= TRAIL_L1_UMMA && g.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
+  if (g.l1_mode < 0 || g.l1_mode > 5) return TRAIL_ERR_INVALID;
+  if (g.l1_mode >= TRAIL_L1_UMMA && g.l1_mode <= TRAIL_L1_WIDE && g.dtype != TRAIL_BF16)
+    return TRAIL_ERR_UNSUPPORTED;
+  if (g.l1_mode == TRAIL_L1_TF32 && g.dtype != TRAIL_F32) return TRAIL_ERR_UNSUPPORTED;
   // every selection runs in one thread-block cluster: 16 x 8192 records (8 x 8192 where a
   // 16-CTA cluster cannot be resident; checked again after select_prepare)
   if ((int64_t)g.max_sched * g.world_size > 16 * 8192) return TRAIL_ERR_CAPACITY;
@@ -339,7 +359,7 @@ trail_status trail_create(const trail_config *cfg, trail_handle *out) {
       cudaMemset(c.xs, 0, (size_t)g.max_requests * c.d * c.esize) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
   if (umma_prepare(c) != cudaSuccess || head_prepare(c) != cudaSuccess ||
-      pool_prepare() != cudaSuccess || gemv_prepare(c) != cudaSuccess ||
+      pool_prepare() != cudaSuccess || gemv_prepare(c) != cudaSuccess || tf32_prepare(c) != cudaSuccess ||
       fused_prepare(c) != cudaSuccess || wide_prepare(c) != cudaSuccess ||
       select_prepare(c) != cudaSuccess)
     return fail(TRAIL_ERR_CUDA);
@@ -392,8 +412,10 @@ trail_status trail_trace_read(trail_handle h, uint64_t *host_out, int32_t max_ct
 }
 
 trail_status trail_set_l1_mode(trail_handle h, int32_t l1_mode) {
-  if (!h || l1_mode < 0 || l1_mode > 4) return TRAIL_ERR_INVALID;
-  if (l1_mode >= TRAIL_L1_UMMA && h->c.dtype != TRAIL_BF16) return TRAIL_ERR_UNSUPPORTED;
+  if (!h || l1_mode < 0 || l1_mode > 5) return TRAIL_ERR_INVALID;
+  if (l1_mode >= TRAIL_L1_UMMA && l1_mode <= TRAIL_L1_WIDE && h->c.dtype != TRAIL_BF16)
+    return TRAIL_ERR_UNSUPPORTED;
+  if (l1_mode == TRAIL_L1_TF32 && h->c.dtype != TRAIL_F32) return TRAIL_ERR_UNSUPPORTED;
   h->c.cfg.l1_mode = l1_mode;
   return TRAIL_OK;
 }
@@ -614,6 +636,9 @@ static trail_status predict_body(Ctx &c, const void *emb, int64_t emb_ld,
   if (mode == TRAIL_L1_GEMV) {
     ProfScope p(c, TRAIL_K_GEMV, s);
     TRAIL_CUDA(launch_gemv_l1(c, emb, emb_ld, row_offsets, n, splits, s));
+  } else if (mode == TRAIL_L1_TF32) {
+    ProfScope p(c, TRAIL_K_GEMV, s);   // (the layer-1 profiling slot of the fp32 path)
+    TRAIL_CUDA(launch_tf32_l1(c, emb, emb_ld, row_offsets, n, s));
   } else {
     ProfScope p(c, TRAIL_K_UMMA, s);
     TRAIL_CUDA(launch_umma_l1(c, n, bn, splits, s));

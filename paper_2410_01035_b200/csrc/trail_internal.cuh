@@ -130,6 +130,11 @@ struct Ctx {
   CUtensorMap tmap_x, tmap_w128, tmap_w256;
   CUtensorMap tmap_w_gemv;                       // W1, 16-byte x 64-row boxes (K2a)
   bool have_tmap_gemv = false;
+  CUtensorMap tmap_w_tf32;                       // fp32 SW128 maps (K2t): W1 128-row boxes,
+  CUtensorMap tmap_xs_tf32[3], tmap_e_tf32[3];   // xs / caller rows in 1-, 4-, 32-row boxes
+  bool have_tmap_tf32 = false;
+  const void *tmap_e_tf32_ptr = nullptr;
+  int64_t tmap_e_tf32_ld = 0;
   CUtensorMap tmap_xs1, tmap_xs4, tmap_xs32;     // xs rows, boxes 64 x {1, 4, 32} (fused gather)
   CUtensorMap tmap_emb, tmap_emb4, tmap_emb32;   // caller's embeddings, same boxes; re-encoded
                                                  // whenever emb / ld change
@@ -202,6 +207,14 @@ cudaError_t launch_release(const Ctx &c, const uint32_t *ids, int n, cudaStream_
 cudaError_t launch_read_state(const Ctx &c, const uint32_t *ids, int n, float *L, uint32_t *age,
                               uint32_t *thr, uint8_t *seen, float *post, cudaStream_t s);
 cudaError_t umma_prepare(Ctx &c);
+// K2t (k_tf32.cu): 3xTF32 tcgen05 layer 1 for fp32 handles
+bool encode_rows_f32_sw128(CUtensorMap *m, const void *base, uint64_t cols, uint64_t rows,
+                           uint64_t ld, uint32_t box_cols, uint32_t box_rows);
+cudaError_t tf32_prepare(Ctx &c);
+bool tf32_supported(const Ctx &c);
+int tf32_splits(const Ctx &c);
+cudaError_t launch_tf32_l1(Ctx &c, const void *emb, int64_t ld, const int32_t *off, int n,
+                           cudaStream_t s);
 bool encode_rows_bf16(CUtensorMap *m, const void *base, uint64_t cols, uint64_t rows, uint64_t ld,
                       uint32_t box_cols, uint32_t box_rows);                // encode tensor maps, set smem attributes
 int umma_max_bn(const Ctx &c);

@@ -30,7 +30,8 @@ TRAIL_ERR_STATE = -6
 TRAIL_ERR_UNSUPPORTED = -7
 
 TRAIL_F32, TRAIL_BF16 = 0, 1
-TRAIL_L1_AUTO, TRAIL_L1_GEMV, TRAIL_L1_UMMA, TRAIL_L1_UMMA_UNFUSED, TRAIL_L1_WIDE = 0, 1, 2, 3, 4
+(TRAIL_L1_AUTO, TRAIL_L1_GEMV, TRAIL_L1_UMMA, TRAIL_L1_UMMA_UNFUSED, TRAIL_L1_WIDE,
+ TRAIL_L1_TF32) = 0, 1, 2, 3, 4, 5
 TRAIL_K = {"pool": 0, "gemv": 1, "umma": 2, "head": 3, "pack": 4, "select": 5, "gather": 6}
 TRAIL_DEV_BAD_ID, TRAIL_DEV_BAD_ROWS, TRAIL_DEV_NEG_KV, TRAIL_DEV_NONFIN = 1, 2, 4, 8
 RECORD_BYTES = 16

@@ -79,12 +79,21 @@ def _cfg(**over):
 @pytest.mark.parametrize("over", [
     dict(k=0), dict(k=33), dict(hidden=500), dict(hidden=640), dict(d=100), dict(dtype=7),
     dict(c=-0.5), dict(c=math.nan), dict(max_slots=0), dict(max_requests=0),
-    dict(world_size=0), dict(l1_mode=5), dict(w1=None),
+    dict(world_size=0), dict(l1_mode=6), dict(l1_mode=-1), dict(w1=None),
 ])
 def test_invalid_configs_rejected_on_host(lib, over):
     cfg, keep = _cfg(**over)
     h = ctypes.c_void_p()
     assert lib.trail_create(ctypes.byref(cfg), ctypes.byref(h)) == T.TRAIL_ERR_INVALID
+    assert not h.value
+
+
+@pytest.mark.parametrize("l1_mode", [T.TRAIL_L1_TF32])
+def test_tf32_mode_needs_fp32(lib, l1_mode):
+    """TRAIL_L1_TF32 (the 3xTF32 tensor-core layer 1) exists for fp32 handles only."""
+    cfg, keep = _cfg(l1_mode=l1_mode)            # a bf16 handle
+    h = ctypes.c_void_p()
+    assert lib.trail_create(ctypes.byref(cfg), ctypes.byref(h)) == T.TRAIL_ERR_UNSUPPORTED
     assert not h.value
 
 

@@ -49,9 +49,37 @@ CASES = [
     ("bf16", 129, 8192, 512, 20, 4, 0.5),    # wide, config 4 width, peer CTA 1 row
     ("bf16", 1000, 1024, 512, 32, 4, 0.1),   # wide, k = 32
     ("bf16", 64, 512, 512, 16, 4, 0.0),      # wide, 8 K blocks (< 2 laps of the ring), empty peer
-    ("f32", 64, 4096, 512, 10, 0, 0.0),      # config 1 shape (fp32 GEMV)
+    ("f32", 64, 4096, 512, 10, 0, 0.0),      # config 1 shape (AUTO -> fp32 GEMV K2a)
+    ("f32", 64, 4096, 512, 10, 5, 0.0),      # config 1 shape on the 3xTF32 tcgen05 kernel K2t
+    ("f32", 64, 4096, 512, 10, 5, 0.3),      # K2t with prompt means from xs
+    ("f32", 130, 1024, 256, 20, 5, 0.1),     # K2t: 3 request blocks (ragged), 2 M tiles
+    ("f32", 9, 4000, 384, 3, 5, 1.0),        # K2t: last K split past d (TMA zero fill), H = 384
     ("f32", 9, 1024, 256, 3, 1, 1.0),
 ]
+
+
+@pytest.mark.parametrize("n,d,H,pf", [(64, 4096, 512, 0.2), (130, 1024, 256, 0.5)])
+def test_tf32_split_matches_fp32_ffma(n, d, H, pf):
+    """K2t's 3xTF32 product (hi*hi + hi*lo + lo*hi, exact hi/lo split) against the fp32 FFMA
+    GEMV K2a on the same fp32 inputs: posteriors within 2e-5 and expected lengths within 1e-5
+    relative — a plain 1xTF32 contraction (10-bit mantissas) misses this by ~100x."""
+    k = 10
+    w = W.make_weights(d, H, k, "f32", seed=3 + n)
+    ids = (np.arange(n) * 2 + 1).astype(np.uint32)
+    outs = []
+    for l1 in (5, 1):
+        t, _ = make_pair(w, 0.8, max_slots=2 * n + 3, max_requests=n, max_sched=n, dtype="f32",
+                         l1_mode=l1)
+        res = []
+        for step in range(2):
+            emb, off, pref = W.make_step_inputs(n, d, "f32", prefill_frac=pf if step else 1.0,
+                                                seed=9, step=step)
+            res.append(gpu_predict(t, emb, off, ids, pref))
+        outs.append(res)
+        t.close()
+    for (qa, La), (qb, Lb) in zip(*outs):
+        assert float(np.abs(qa - qb).max()) <= 2e-5
+        assert float((np.abs(La - Lb) / Lb).max()) <= 1e-5
 
 
 @pytest.mark.parametrize("dtype,n,d,H,k,l1,pf", CASES)
