@@ -192,7 +192,7 @@ size_t partial_elems_needed(const Ctx &c) {
       tmp_c.cfg = c.cfg;
       // bf16: the GEMV and unfused tcgen05 plans; fp32: the GEMV and 3xTF32 plans
       tmp_c.cfg.l1_mode = forced ? TRAIL_L1_GEMV
-                                 : (c.dtype == TRAIL_F32 ? TRAIL_L1_AUTO : TRAIL_L1_UMMA_UNFUSED);
+                                 : (c.dtype == TRAIL_F32 ? TRAIL_L1_TF32 : TRAIL_L1_UMMA_UNFUSED);
       tmp_c.d = c.d; tmp_c.H = c.H; tmp_c.dtype = c.dtype; tmp_c.num_sms = c.num_sms;
       int mode, bn, s;
       plan_l1(tmp_c, n, &mode, &bn, &s, true);

@@ -3,9 +3,9 @@ compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
 
     compute-sanitizer --tool memcheck python scripts/sanitize.py
 
-Covers: K1 pooling (register and bulk variants), K2a GEMV + K3 head, K2c split-K tcgen05
-(fused head), K2d CTA-pair tcgen05, K4 selection as a 1-CTA and as a multi-CTA cluster
-(local build and given records with padding), K5 pack, K6 time update, K1c chunked prefill,
+Covers: K1 pooling (register and bulk variants), K2a GEMV + K3 head, K2t 3xTF32 tcgen05 + K3,
+K2c split-K tcgen05 (fused head), K2d CTA-pair tcgen05, K4 selection by rank counting and by
+the bucketed sample sort (local build and given records with padding), K5 pack, K6 time update, K1c chunked prefill,
 K1m multi-layer mix, release and state read.  Exits non-zero on a CUDA error; the sanitizer
 reports its own findings."""
 import os
@@ -72,9 +72,10 @@ def run(n, d, dtype, l1_mode, waiting):
 def main():
     torch.cuda.init()
     run(24, 1024, "f32", 1, 8)        # GEMV + head (fp32)
+    run(70, 1024, "f32", 5, 8)        # K2t 3xTF32 tcgen05 (two request blocks) + head
     run(40, 1024, "bf16", 2, 10)      # K2c split-K tcgen05
-    run(300, 1024, "bf16", 4, 100)    # K2d CTA pair; selection as one CTA
-    run(600, 512, "bf16", 2, 4000)    # selection as a multi-CTA cluster (4600 records)
+    run(300, 1024, "bf16", 4, 100)    # K2d CTA pair; rank-counting selection (<= 2048 records)
+    run(600, 512, "bf16", 2, 4000)    # bucketed sample-sort selection (4600 records)
     print("sanitize workload done")
 
 
