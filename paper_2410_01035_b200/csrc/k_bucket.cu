@@ -228,11 +228,14 @@ trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, const BkKey *__r
                          unsigned long long *__restrict__ forced_tot,
                          uint16_t *__restrict__ bkid, uint64_t *__restrict__ trace) {
   __shared__ BkKey spl[kB];
-  __shared__ uint32_t h_cnt[kB], h_run[kB];
-  __shared__ unsigned long long h_kv[kB];
+  // KV per bucket as two 32-bit halves (native shared-memory atomics; a 64-bit shared atomic
+  // add is a CAS loop on this part)
+  __shared__ uint32_t h_cnt[kB], h_run[kB], h_klo[kB], h_khi[kB];
   uint64_t *tr = trace ? trace + 16 * (kTrB1 + (int64_t)blockIdx.x) : nullptr;   // diagnostics
   if (tr && threadIdx.x == 0) tr[0] = ptx::gtimer();
-  for (int q = threadIdx.x; q < kB; q += kB1Threads) { h_cnt[q] = 0u; h_run[q] = 0u; h_kv[q] = 0ull; }
+  for (int q = threadIdx.x; q < kB; q += kB1Threads) {
+    h_cnt[q] = 0u; h_run[q] = 0u; h_klo[q] = 0u; h_khi[q] = 0u;
+  }
   griddep_wait();     // splitters (and local records) from B0
   griddep_launch();
   if (tr && threadIdx.x == 0) tr[1] = ptx::gtimer();
@@ -251,7 +254,8 @@ trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, const BkKey *__r
         frc = (v.x >> 31) == 0u ? 1u : 0u;
         atomicAdd(&h_cnt[b], 1u);
         if (v.w >> 31) atomicAdd(&h_run[b], 1u);
-        atomicAdd(&h_kv[b], (unsigned long long)kvv);
+        atomicAdd(&h_klo[b], kvv & 0xFFFFu);
+        if (kvv >> 16) atomicAdd(&h_khi[b], kvv >> 16);
       }
       bkid[i] = (uint16_t)(b < 0 ? 0xFFFF : b);   // reused by B2 (no second search)
     }
@@ -267,7 +271,7 @@ trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, const BkKey *__r
     if (h_cnt[q]) {
       atomicAdd(hcnt + q, h_cnt[q]);
       if (h_run[q]) atomicAdd(hrun + q, h_run[q]);
-      atomicAdd(hkv + q, h_kv[q]);
+      atomicAdd(hkv + q, ((unsigned long long)h_khi[q] << 16) + h_klo[q]);
     }
   if (tr && threadIdx.x == 0) tr[2] = ptx::gtimer();
 }
@@ -422,7 +426,7 @@ trail_bucket_rank_kernel(const Record *__restrict__ rec, int m, uint32_t *__rest
   if (t == 0) {
     const unsigned long long inc = (1ull << 48) | ((unsigned long long)s_run << 24) | s_rcut;
     unsigned long long old;
-    asm volatile("atom.add.acq_rel.gpu.u64 %0, [%1], %2;" : "=l"(old) : "l"(gcnt), "l"(inc) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(gcnt), "l"(inc) : "memory");
     const unsigned long long tot = old + inc;
     s_last = (int)(tot >> 48) == (int)gridDim.x ? 1 : 0;
     if (s_last) *gcnt = 0ull;

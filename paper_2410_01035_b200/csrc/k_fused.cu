@@ -382,7 +382,7 @@ trail_fused_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
     uint32_t *cnt = arrive_cnt + (int64_t)blockIdx.x * MAXS + crank;
     uint32_t old;
     // release: this CTA's z_part stores (ordered before it by the barrier)
-    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
     if (spin) {
       const uint32_t target = (old / (uint32_t)NT + 1u) * (uint32_t)NT;   // monotone epochs
       uint32_t cur = old + 1u;

@@ -294,7 +294,7 @@ trail_select_rank_kernel(const Record *__restrict__ rec_in, Record *__restrict__
     const unsigned long long inc = (1ull << 48) | ((unsigned long long)s_cta_run << 24) |
                                    (unsigned long long)s_cta_rcut;
     unsigned long long old;
-    asm volatile("atom.add.acq_rel.gpu.u64 %0, [%1], %2;"
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;"
                  : "=l"(old) : "l"(gcnt), "l"(inc) : "memory");
     const unsigned long long tot = old + inc;
     sh.last = (int)(tot >> 48) == (int)gridDim.x ? 1 : 0;
