@@ -49,21 +49,6 @@ constexpr int OFF_XLO = 2 * W_BYTES + X_BYTES;
 constexpr int OFF_BAR = 2 * W_BYTES + 2 * X_BYTES;
 constexpr int TSMEM = OFF_BAR + 64 + 1024;  // + slack for 1024-byte alignment
 
-// instruction descriptor, kind::tf32: D fp32, A/B tf32, both K-major, M x N
-__host__ __device__ constexpr uint32_t idesc_tf32_f32(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(M >> 4) << 24);
-}
-
-__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                          uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accum));
-}
-
 // x -> (hi, lo) in place: hi over x, lo into the twin tile at the same offset
 __device__ __forceinline__ void split_tf32(uint8_t *hi, uint8_t *lo, int bytes) {
   for (int v = threadIdx.x; v < bytes / 16; v += TT) {

@@ -23,8 +23,9 @@
 // buffer (7 x 16 KB: 191 -> 179 us per launch).  Deeper or batched X requests (8 stages,
 // 4 K blocks per request group) and L2 prefetch of the X rows ahead of the ring were
 // measured slower.
-//   all 8 warps   : epilogue — TMEM (lane = row) -> +b1, ReLU -> layer-2 partials over two
-//                   column halves (fixed order) -> head, one lane per bin (head_dev.cuh)
+//   all 8 warps   : epilogue — TMEM (lane = row) -> +b1, ReLU -> layer 2 on the tensor cores
+//                   (3xTF32 pair MMA, M = 256, N = 16/32 bins, 16 chunks of 32 hidden units,
+//                   4 A buffers) -> head, one lane per bin (head_dev.cuh)
 #include <math.h>
 #include <stdlib.h>
 
@@ -61,10 +62,10 @@ struct WCfg {
   static constexpr int HC_OFF = LQ_OFF + WBM * KB * 4;
   static constexpr int SMEM_USED = HC_OFF + (int)sizeof(HeadSmem);
   static constexpr int SMEM_TOTAL = SMEM_USED + 1024;
-  // after the mainloop the pipeline buffers hold W2^T [512][KBP] and z [2][128][KBP]
-  static constexpr int W2S_OFF = 0;
-  static constexpr int ZS_OFF = WH * KBP * 4;
-  static_assert(ZS_OFF + 2 * WBM * KBP * 4 <= PIPE, "epilogue staging must fit the pipeline");
+  // after the mainloop the pipeline buffers hold W2 hi / lo (2 x 32 KB), the layer-2 A tiles
+  // (2 x 32 KB) and z [128][KBP]
+  static_assert(2 * 16 * 2048 + 4 * 32768 <= PIPE, "epilogue staging must fit");
+  static_assert(8 * (2 * XS + 2 * WS + 1) + 8 <= 176, "barrier block");
   static_assert(SMEM_TOTAL <= 232448, "shared memory budget");
 };
 }  // namespace
@@ -102,8 +103,6 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
   SlotMeta *s_meta = reinterpret_cast<SlotMeta *>(smem + C::META_OFF);
   float *s_lq = reinterpret_cast<float *>(smem + C::LQ_OFF);
   HeadSmem &hs = *reinterpret_cast<HeadSmem *>(smem + C::HC_OFF);
-  float *w2s = reinterpret_cast<float *>(smem + C::W2S_OFF);   // [512][KBP] after the mainloop
-  float *zs = reinterpret_cast<float *>(smem + C::ZS_OFF);     // [2][128][KBP]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const uint32_t r = cluster_rank();
@@ -119,6 +118,12 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
       mbar_init(wfull0 + 8 * i, 1);
       mbar_init(wempty0 + 8 * i, 1);
     }
+    // layer-2 barriers (epilogue): afull[4] (4 producer warps x 2 CTAs), afree[4], zdone
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(s0 + C::BAR_OFF + 176 + 8 * i, 8);
+      mbar_init(s0 + C::BAR_OFF + 208 + 8 * i, 1);
+    }
+    mbar_init(s0 + C::BAR_OFF + 240, 1);
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_w)) : "memory");
@@ -234,43 +239,104 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
   }
 
   // ---- epilogue: the pipeline is idle once `done` completes (all MMAs of the pair retired)
+  constexpr int NB = KB <= 16 ? 16 : 32;           // layer-2 MMA N (bins padded)
+  constexpr int BH = NB / 2;                       // bins held by this CTA (B split of the pair)
+  constexpr int W2PER = BH * WH / WT;              // W2 values per thread
+  // this CTA's W2 rows into registers while the last MMAs run (L2 latency off the tail)
+  float w2r[W2PER];
+#pragma unroll
+  for (int u = 0; u < W2PER; ++u) {
+    const int v = tid + u * WT, bl = v / WH, x = v - bl * WH, bin = (int)r * BH + bl;
+    w2r[u] = bin < k ? __ldg(w2 + (int64_t)bin * WH + x) : 0.f;
+  }
   mbar_wait(done, 0);
   __syncwarp();
   tc_fence_after();
-  // W2^T into the idle pipeline buffers: w2s[c][b] = W2[b][c] (b >= k zero), coalesced reads
-  for (int v = tid; v < KBP * WH; v += WT) {
-    const int b = v / WH, c = v - b * WH;
-    w2s[c * KBP + b] = b < k ? __ldg(w2 + (int64_t)b * WH + c) : 0.f;
+  // ---- layer 2 on the tensor cores (3xTF32, exact hi/lo split): z[256 x NB] = h W2^T over the
+  // pair (M = 256, N = NB bins padded, K = 512 hidden in 16 chunks of 32).  The FFMA version
+  // (128 x 512 x 20 FMAs per CTA on the CUDA cores) cost ~18 us of the kernel (probe).
+  //   W2 -> this CTA's NB/2 bins of every chunk, split into TF32 hi / fp32 lo, K-major SW128
+  //   producers: warps w and w + 4 own TMEM lanes 32 (w & 3) ..; warps 0-3 build the even
+  //   chunks, 4-7 the odd ones: h = ReLU(acc + b1) from TMEM -> hi / lo A tiles (4 buffers)
+  //   MMA issue: thread 0 of the leader, in chunk order, 3 MMAs per 8 columns of K
+  //   (hi.hi + hi.lo + lo.hi); the accumulator takes TMEM columns [0, NB) once chunk 0 (those
+  //   columns of h) has been read by every producer.
+  constexpr int W2T = 2048;                        // bytes per chunk of B (hi or lo)
+  constexpr int NA = 4;                            // A buffers (32 KB each: hi + lo)
+  const uint32_t w2hi = s0, w2lo = s0 + 16 * W2T, abuf = s0 + 32 * W2T;
+  const uint32_t ebar = s0 + C::BAR_OFF + 176;     // afull[NA] (8 arrivals), afree[NA], zdone
+  const uint32_t afull0 = ebar, afree0 = ebar + 8 * NA, zdone = ebar + 16 * NA;
+#pragma unroll
+  for (int u = 0; u < W2PER; ++u) {
+    const int v = tid + u * WT, bl = v / WH, x = v - bl * WH;
+    const float val = w2r[u];
+    const float hi = tf32_hi(val);
+    const int kk = x & 31;
+    const uint32_t off = (uint32_t)((x >> 5) * W2T + (bl >> 3) * 1024 + (bl & 7) * 128 +
+                                    (((kk >> 2) ^ (bl & 7)) << 4) + (kk & 3) * 4);
+    *reinterpret_cast<float *>(smem + off) = hi;
+    *reinterpret_cast<float *>(smem + 16 * W2T + off) = val - hi;
   }
+  fence_proxy_async_smem();
   __syncthreads();
   {
-    // thread (row, column half): h = ReLU(acc + b1) over 256 columns, z_half = W2 h_half
-    const int g = warp & 3, half = warp >> 2;
-    const int row = 32 * g + lane;
-    float z[KBP];
+    constexpr uint32_t idesc2 = idesc_tf32_f32(2 * WBM, NB);
+    auto issue = [&](int cc) {                     // leader, thread 0
+      const int bf = cc % NA;
+      mbar_wait(afull0 + 8 * bf, (uint32_t)(cc / NA) & 1u);
+      tc_fence_after();
+      const uint64_t ah = sw128_kmajor_desc(abuf + bf * 32768), al = sw128_kmajor_desc(abuf + bf * 32768 + 16384);
+      const uint64_t bh = sw128_kmajor_desc(w2hi + cc * W2T), bl = sw128_kmajor_desc(w2lo + cc * W2T);
 #pragma unroll
-    for (int b = 0; b < KBP; ++b) z[b] = 0.f;
-    for (int cc = 0; cc < 256; cc += 32) {
-      const int c0 = 256 * half + cc;
-      uint32_t v[32];
-      tmem_ld32(tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)c0, v);
-#pragma unroll 4
-      for (int q = 0; q < 32; ++q) {
-        const float hq = fmaxf(__uint_as_float(v[q]) + b1s[c0 + q], 0.f);
-        const float4 *wq = reinterpret_cast<const float4 *>(w2s + (c0 + q) * KBP);
-#pragma unroll
-        for (int b4 = 0; b4 < KBP / 4; ++b4) {
-          const float4 w = wq[b4];
-          z[4 * b4] = fmaf(hq, w.x, z[4 * b4]);
-          z[4 * b4 + 1] = fmaf(hq, w.y, z[4 * b4 + 1]);
-          z[4 * b4 + 2] = fmaf(hq, w.z, z[4 * b4 + 2]);
-          z[4 * b4 + 3] = fmaf(hq, w.w, z[4 * b4 + 3]);
-        }
+      for (int kk = 0; kk < 4; ++kk) {             // +32 bytes along K per 8 fp32
+        umma_tf32_pair(tmem, ah + 2 * kk, bh + 2 * kk, idesc2, (cc > 0 || kk > 0) ? 1u : 0u);
+        umma_tf32_pair(tmem, ah + 2 * kk, bl + 2 * kk, idesc2, 1u);
+        umma_tf32_pair(tmem, al + 2 * kk, bh + 2 * kk, idesc2, 1u);
       }
-    }
-    float4 *zo = reinterpret_cast<float4 *>(zs + (half * WBM + row) * KBP);
+      umma_commit_pair(afree0 + 8 * bf);
+    };
+    const int g = warp & 3, par = warp >> 2, row = 32 * g + lane;
+    const int rb = (row >> 3) * 1024 + (row & 7) * 128;
+    for (int c = par; c < WH / 32; c += 2) {
+      const int bf = c % NA;
+      if (c >= NA) mbar_wait(afree0 + 8 * bf, (uint32_t)(c / NA - 1) & 1u);
+      uint32_t v[32];
+      tmem_ld32(tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)(32 * c), v);
+      uint8_t *ahi = smem + 32 * W2T + bf * 32768, *alo = ahi + 16384;
 #pragma unroll
-    for (int b4 = 0; b4 < KBP / 4; ++b4) zo[b4] = make_float4(z[4 * b4], z[4 * b4 + 1], z[4 * b4 + 2], z[4 * b4 + 3]);
+      for (int q4 = 0; q4 < 8; ++q4) {
+        float h[4], hh[4], hl[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          h[e] = fmaxf(__uint_as_float(v[4 * q4 + e]) + b1s[32 * c + 4 * q4 + e], 0.f);
+          hh[e] = tf32_hi(h[e]);
+          hl[e] = h[e] - hh[e];
+        }
+        const int off = rb + ((q4 ^ (row & 7)) << 4);
+        *reinterpret_cast<float4 *>(ahi + off) = make_float4(hh[0], hh[1], hh[2], hh[3]);
+        *reinterpret_cast<float4 *>(alo + off) = make_float4(hl[0], hl[1], hl[2], hl[3]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa(afull0 + 8 * bf, 0u));
+      if (r == 0 && warp == 0 && lane == 0)
+        for (int cc = c > 0 ? c - 1 : 0; cc <= c; ++cc) issue(cc);
+      __syncwarp();
+    }
+    if (r == 0 && tid == 0) {
+      issue(WH / 32 - 1);
+      umma_commit_pair(zdone);
+    }
+  }
+  mbar_wait(zdone, 0);
+  tc_fence_after();
+  float *zs2 = reinterpret_cast<float *>(smem + 32 * W2T);   // [WBM][KBP] over A buffer 0
+  if (warp < 4) {
+    uint32_t v[32];
+    tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16), v);
+#pragma unroll
+    for (int b = 0; b < KBP; ++b) zs2[(32 * warp + lane) * KBP + b] = __uint_as_float(v[b]);
   }
   __syncthreads();
   // ---- head (row a3): one lane per bin, SEG-lane segments, rows spread over the 8 warps
@@ -282,7 +348,7 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
       const int j = m0 + rr < n ? m0 + rr : n;
       float z = 0.f;
       if (j < n && b < k)
-        z = (__ldg(b2 + b) + zs[rr * KBP + b]) + zs[(WBM + rr) * KBP + b];
+        z = __ldg(b2 + b) + zs2[rr * KBP + b];
       head_seg(j, n, k, SEG, b, z, hs, cst.dyn_c, j < n ? s_slot[rr] : 0xFFFFFFFFu, s_meta[rr],
                b < KB ? s_lq[rr * KB + (b < KB ? b : 0)] : -INFINITY, prior_override, lq_state,
                meta, post, Lout, err);

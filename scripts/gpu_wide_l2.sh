@@ -1,0 +1,6 @@
+mkdir -p gpurun_out; rm -f gpurun_out/wide_l2.log
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x --timeout 120 -p no:cacheprovider -k "4-0 or 4-0. or wide or smoke" >> gpurun_out/wide_l2.log 2>&1
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -m gpu --timeout 120 -p no:cacheprovider -k "predict_two_steps" >> gpurun_out/wide_l2.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_fullsize.py -q -m gpu -x --timeout 300 -p no:cacheprovider >> gpurun_out/wide_l2.log 2>&1
+timeout 300 python scripts/wide_probe.py >> gpurun_out/wide_l2.log 2>&1
+grep -v "^\.\|^$" gpurun_out/wide_l2.log | tail -20
