@@ -42,7 +42,7 @@ constexpr int kS = kB;                  //  is a splitter)
 constexpr int kB0Threads = 1024;
 constexpr int kB1Threads = 1024;
 constexpr int kB3Threads = 1024;
-constexpr int kB3Tpi = 8;               // threads per record in B3
+constexpr int kB3Tpi = 4;               // threads per record in B3 (256 records per CTA)
 constexpr int kB3Items = kB3Threads / kB3Tpi;
 constexpr int kStageCap = 4096;         // bucket entries staged in shared memory (64 KB)
 // per-CTA phase traces (trail_trace_*, diagnostics): trace rows of B3, B0, B1, B2
@@ -66,19 +66,6 @@ __device__ __forceinline__ bool bk_lt(unsigned long long ka, uint32_t ia, unsign
 
 __device__ __forceinline__ bool bk_less(const BkEntry &a, const BkEntry &b) {
   return bk_lt(a.key, a.idx, b.key, b.idx);
-}
-
-// bucket = number of splitters <= (key, idx): binary search over kB - 1 splitters in smem
-__device__ __forceinline__ int bk_bucket(const BkKey *__restrict__ spl, unsigned long long key,
-                                         uint32_t idx) {
-  int lo = 0, hi = kB - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    const BkKey sp = spl[mid];
-    if (!bk_lt(key, idx, sp.key, sp.idx)) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
 }
 
 __device__ __forceinline__ unsigned long long rec_key(uint32_t keybits, uint32_t arrival) {
@@ -227,7 +214,9 @@ trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, const BkKey *__r
                          unsigned long long *__restrict__ hkv,
                          unsigned long long *__restrict__ forced_tot,
                          uint16_t *__restrict__ bkid, uint64_t *__restrict__ trace) {
-  __shared__ BkKey spl[kB];
+  // splitters as separate key / index arrays: the search's (divergent) loads are 8 + 4 bytes
+  __shared__ unsigned long long spl_k[kB];
+  __shared__ uint32_t spl_i[kB];
   // KV per bucket as two 32-bit halves (native shared-memory atomics; a 64-bit shared atomic
   // add is a CAS loop on this part)
   __shared__ uint32_t h_cnt[kB], h_run[kB], h_klo[kB], h_khi[kB];
@@ -239,7 +228,11 @@ trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, const BkKey *__r
   griddep_wait();     // splitters (and local records) from B0
   griddep_launch();
   if (tr && threadIdx.x == 0) tr[1] = ptx::gtimer();
-  for (int q = threadIdx.x; q < kB - 1; q += kB1Threads) spl[q] = spl_g[q];
+  for (int q = threadIdx.x; q < kB - 1; q += kB1Threads) {
+    const BkKey sp = spl_g[q];
+    spl_k[q] = sp.key;
+    spl_i[q] = sp.idx;
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   for (int i0 = blockIdx.x * kB1Threads; i0 < m; i0 += gridDim.x * kB1Threads) {
@@ -249,7 +242,17 @@ trail_bucket_hist_kernel(const Record *__restrict__ rec, int m, const BkKey *__r
       const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(rec + i));
       int b = -1;
       if (v.x != kPadKey) {
-        b = bk_bucket(spl, rec_key(v.x, v.y), (uint32_t)i);
+        {   // bucket = number of splitters <= (key, i)
+          const unsigned long long key = rec_key(v.x, v.y);
+          int lo = 0, hi = kB - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const unsigned long long sk = spl_k[mid];
+            if (sk < key || (sk == key && spl_i[mid] <= (uint32_t)i)) lo = mid + 1;
+            else hi = mid;
+          }
+          b = lo;
+        }
         kvv = v.z;
         frc = (v.x >> 31) == 0u ? 1u : 0u;
         atomicAdd(&h_cnt[b], 1u);
