@@ -58,6 +58,33 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("n,d,k,pf", [(300, 4096, 10, 0.2), (520, 8192, 20, 0.05), (260, 1024, 32, 0.5)])
+def test_wide_tensor_core_layer2_matches_fused(n, d, k, pf):
+    """K2d computes layer 2 on the tensor cores (3xTF32 pair MMA over an exact hi/lo split of
+    h and W2); K2c computes it in fp32 FFMA.  Same bf16 inputs, same layer-1 arithmetic up to
+    summation order (K2c splits K over a cluster): posteriors within 2e-5 — a plain 1xTF32
+    or bf16 layer 2 misses this by two orders of magnitude — and expected lengths within
+    1e-4 relative (|dL| <= sum_i |dq_i| m_i with bin middles up to ~1000: the q bound
+    carried over, still 10x inside the BASELINE 1e-3)."""
+    edges = W.paper_bin_edges(k) if k != 20 else W.paper_bin_edges(20, 1024.0)
+    w = W.make_weights(d, 512, k, "bf16", edges=edges, seed=21 + n)
+    ids = (np.arange(n) * 2 + 1).astype(np.uint32)
+    outs = []
+    for l1 in (4, 2):
+        t, _ = make_pair(w, 0.8, max_slots=2 * n + 3, max_requests=n, max_sched=n, dtype="bf16",
+                         l1_mode=l1)
+        res = []
+        for step in range(2):
+            emb, off, pref = W.make_step_inputs(n, d, "bf16", prefill_frac=pf if step else 1.0,
+                                                seed=13, step=step)
+            res.append(gpu_predict(t, emb, off, ids, pref))
+        outs.append(res)
+        t.close()
+    for (qa, La), (qb, Lb) in zip(*outs):
+        assert float(np.abs(qa - qb).max()) <= 2e-5
+        assert float((np.abs(La - Lb) / Lb).max()) <= 1e-4
+
+
 @pytest.mark.parametrize("n,d,H,pf", [(64, 4096, 512, 0.2), (130, 1024, 256, 0.5)])
 def test_tf32_split_matches_fp32_ffma(n, d, H, pf):
     """K2t's 3xTF32 product (hi*hi + hi*lo + lo*hi, exact hi/lo split) against the fp32 FFMA
