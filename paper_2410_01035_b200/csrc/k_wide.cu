@@ -165,25 +165,28 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
                           &tmap_emb4, &tmap_emb32, &tmap_xs, &tmap_xs4, &tmap_xs32);
     }
   } else if (warp == 2) {
-    // ---- W1 producer (lane 0): my halves of the two N = 256 column blocks into the W1 ring;
-    // W1 does not depend on an earlier kernel, so the first stages overlap its tail (PDL)
-    if (lane == 0) {
-      const uint32_t lead_wfull0 = mapa(wfull0, 0u);
-      const uint32_t w_tx = skip_w ? 0u : (uint32_t)(4 * WBH);
-      for (int i = 0; i < kblocks; ++i) {
-        const int st = i % WS;
-        if (i >= WS) mbar_wait(wempty0 + 8 * st, ((uint32_t)(i / WS) & 1u) ^ 1u);
+    // ---- W1 producer (the converged warp, one elected lane issues): my halves of the two
+    // N = 256 column blocks into the W1 ring; W1 does not depend on an earlier kernel, so the
+    // first stages overlap its tail (PDL)
+    const uint32_t lead_wfull0 = mapa(wfull0, 0u);
+    const uint32_t w_tx = skip_w ? 0u : (uint32_t)(4 * WBH);
+    for (int i = 0; i < kblocks; ++i) {
+      const int st = i % WS;
+      if (i >= WS) mbar_wait(wempty0 + 8 * st, ((uint32_t)(i / WS) & 1u) ^ 1u);
+      const uint32_t sb = s0 + XS * WA + st * 2 * WBH;
+      if (elect_one()) {
         if (r == 0) mbar_expect_tx(wfull0 + 8 * st, w_tx);
-        const uint32_t sb = s0 + XS * WA + st * 2 * WBH;
         if (!skip_w) {
           tma_load_2d_pair(sb, &tmap_w, lead_wfull0 + 8 * st, i * WBK, (int)r * 128);
           tma_load_2d_pair(sb + WBH, &tmap_w, lead_wfull0 + 8 * st, i * WBK, 256 + (int)r * 128);
         }
       }
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0 && r == 0) {
+    // ---- MMA issue (leader CTA): the whole warp walks the K loop (waits, descriptors: all
+    // warp-uniform), one elected lane issues the MMAs and commits
+    if (r == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(2 * WBM, 256);
       for (int i = 0; i < kblocks; ++i) {
         const int sx = i % XS, sw = i % WS;
@@ -192,19 +195,22 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
         tc_fence_after();
         const uint64_t da = sw128_kmajor_desc(s0 + sx * WA);
         const uint32_t sb = s0 + XS * WA + sw * 2 * WBH;
+        if (elect_one()) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint64_t db = sw128_kmajor_desc(sb + h * WBH);
+          for (int h = 0; h < 2; ++h) {
+            const uint64_t db = sw128_kmajor_desc(sb + h * WBH);
 #pragma unroll
-          for (int kk = 0; kk < WBK / 16; ++kk)
-            umma_bf16_pair(tmem + 256 * h, da + 2 * kk, db + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < WBK / 16; ++kk)
+              umma_bf16_pair(tmem + 256 * h, da + 2 * kk, db + 2 * kk, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit_pair(xempty0 + 8 * sx);
+          umma_commit_pair(wempty0 + 8 * sw);
         }
-        umma_commit_pair(xempty0 + 8 * sx);
-        umma_commit_pair(wempty0 + 8 * sw);
+        __syncwarp();
       }
-      umma_commit_pair(done);
+      if (elect_one()) umma_commit_pair(done);
+      __syncwarp();
     }
-    __syncwarp();
   } else {
     // warps 3-7: b1, head constants and this CTA's slot state (weights and state written by
     // kernels that completed before the pool kernel passed its own griddep_wait: PDL chain)

@@ -201,6 +201,18 @@ __device__ __forceinline__ void umma_tf32_pair(uint32_t tmem_d, uint64_t a, uint
       "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
+// one lane of a converged warp (elect.sync): instructions that take uniform operands (tcgen05.mma,
+// TMA) issued under it keep their warp-uniform operands in uniform registers, where a
+// `lane == 0` branch makes the compiler wrap each one in an ELECT / R2UR waterfall loop
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, e;\n\t}\n"
+      : "=r"(p));
+  return p != 0;
+}
 // exact split of an fp32 value into a TF32 head (13 low mantissa bits cleared) and the fp32
 // remainder: x = hi + lo exactly
 __device__ __forceinline__ float tf32_hi(float x) {
