@@ -113,4 +113,95 @@ __device__ __forceinline__ void head_seg(int j, int n, int k, int SEG, int b, fl
   }
 }
 
+
+// Row a3 head for request j by ONE thread over all k bins (same recursion as head_seg, the
+// reductions sequential in bin order instead of shuffle trees): no cross-lane dependency
+// chains, so 128 rows run as 128 independent threads.  K2d's epilogue (128 rows per CTA)
+// measured 23 us with head_seg (one warp per row: five dependent shuffle reductions per
+// row, 16 rows per warp in sequence).
+template <int KB>
+__device__ __forceinline__ void head_row(int j, int k, const float (&z)[KB], const HeadSmem &hc,
+                                         float hc_dyn_c, uint32_t sl, const SlotMeta &mt,
+                                         const float *__restrict__ lq_prev,
+                                         const float *__restrict__ prior_override,
+                                         float *__restrict__ lq_state, SlotMeta *__restrict__ meta,
+                                         float *__restrict__ post, float *__restrict__ Lout,
+                                         uint32_t *__restrict__ err) {
+  if (sl == 0xFFFFFFFFu) {
+    atomicOr(err, TRAIL_DEV_BAD_ID);
+    if (post)
+      for (int b = 0; b < k; ++b) post[(int64_t)j * k + b] = NAN;
+    if (Lout) Lout[j] = NAN;
+    return;
+  }
+  const uint32_t slot = sl & 0x7FFFFFFFu;
+  const bool first = (sl >> 31) != 0u || !(mt.flags & 1u);
+  float zmax = -INFINITY;
+#pragma unroll
+  for (int b = 0; b < KB; ++b) if (b < k) zmax = fmaxf(zmax, z[b]);
+  float se = 0.f;
+#pragma unroll
+  for (int b = 0; b < KB; ++b) if (b < k) se += __expf(z[b] - zmax);
+  const float lse = zmax + __logf(se);
+  float lp[KB], lq[KB];
+#pragma unroll
+  for (int b = 0; b < KB; ++b) {
+    lp[b] = b < k ? z[b] - lse : -INFINITY;
+    float lpr = -INFINITY;
+    if (b < k) {
+      if (first) {
+        lpr = prior_override ? __logf(__ldg(prior_override + (int64_t)j * k + b)) : hc.log_prior[b];
+      } else {
+        // prior(b) = (1 - 1/w_b) q(b) + (1/w_{b+1}) q(b+1): T applied to the posterior (D-1, D-2)
+        const float stay = hc.log_stay[b] + lq_prev[b];
+        const float move = b + 1 < k ? hc.log_move[b] + lq_prev[b + 1 < KB ? b + 1 : b] : -INFINITY;
+        const float mx = fmaxf(stay, move), mn = fminf(stay, move);
+        lpr = mx == -INFINITY ? -INFINITY : mx + __logf(1.f + __expf(mn - mx));
+      }
+    }
+    lq[b] = lpr + lp[b];
+  }
+  // (max, argmax) of the unnormalised log q and of log p (D-5 fallback), lowest index on ties
+  float qmax = -INFINITY, pmax = -INFINITY;
+  int bi = 0, pi = 0;
+#pragma unroll
+  for (int b = 0; b < KB; ++b)
+    if (b < k) {
+      if (lq[b] > qmax) { qmax = lq[b]; bi = b; }
+      if (lp[b] > pmax) { pmax = lp[b]; pi = b; }
+    }
+  if (qmax == -INFINITY) {          // all-zero product: fall back to p (D-5)
+#pragma unroll
+    for (int b = 0; b < KB; ++b) lq[b] = lp[b];
+    qmax = pmax;
+    bi = pi;
+  }
+  float qs = 0.f;
+#pragma unroll
+  for (int b = 0; b < KB; ++b) if (b < k) qs += __expf(lq[b] - qmax);
+  const float lnorm = qmax + __logf(qs);
+  float L = 0.f;
+#pragma unroll
+  for (int b = 0; b < KB; ++b)
+    if (b < k) {
+      const float l = lq[b] - lnorm;
+      const float q = __expf(l);
+      L += q * hc.m[b];
+      lq_state[(int64_t)slot * k + b] = l;
+      if (post) post[(int64_t)j * k + b] = q;
+    }
+  SlotMeta o = mt;
+  if (first) {
+    o.thr = hc.thr[bi];
+    o.age = 0;
+    o.flags = 1u;
+  } else {
+    o.age += 1;
+  }
+  o.L = L;
+  if (hc_dyn_c >= 0.f) o.thr = dynamic_threshold(hc_dyn_c, L);
+  meta[slot] = o;
+  if (Lout) Lout[j] = L;
+}
+
 }  // namespace trail

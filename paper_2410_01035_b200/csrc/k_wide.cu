@@ -86,7 +86,8 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
                           const float *__restrict__ prior_override, int max_slots,
                           float *__restrict__ lq_state, SlotMeta *__restrict__ meta,
                           float *__restrict__ post, float *__restrict__ Lout,
-                          uint32_t *__restrict__ err, int decode_only, int wflags) {
+                          uint32_t *__restrict__ err, int decode_only, int wflags,
+                          uint64_t *__restrict__ trace) {
   using C = WCfg<KB>;
   constexpr int KBP = C::KBP;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -106,6 +107,8 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const uint32_t r = cluster_rank();
+  uint64_t *tr = trace ? trace + 16 * (int64_t)blockIdx.x : nullptr;   // diagnostics (trail_trace_*)
+  if (tr && tid == 0) tr[0] = gtimer();
   const int m0 = (int)(blockIdx.x >> 1) * 2 * WBM + (int)r * WBM;
   const int k = cst.k;
 
@@ -135,6 +138,7 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   griddep_launch();
+  if (tr && tid == 0) tr[1] = gtimer();
 
   if (warp == 0) {
     // ---- X producer (all lanes: the row gather of xgather.cuh) into the X ring.  X streams
@@ -258,13 +262,15 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
   mbar_wait(done, 0);
   __syncwarp();
   tc_fence_after();
+  if (tr && tid == 0) tr[2] = gtimer();
   // ---- layer 2 on the tensor cores (3xTF32, exact hi/lo split): z[256 x NB] = h W2^T over the
   // pair (M = 256, N = NB bins padded, K = 512 hidden in 16 chunks of 32).  The FFMA version
   // (128 x 512 x 20 FMAs per CTA on the CUDA cores) cost ~18 us of the kernel (probe).
   //   W2 -> this CTA's NB/2 bins of every chunk, split into TF32 hi / fp32 lo, K-major SW128
   //   producers: warps w and w + 4 own TMEM lanes 32 (w & 3) ..; warps 0-3 build the even
   //   chunks, 4-7 the odd ones: h = ReLU(acc + b1) from TMEM -> hi / lo A tiles (4 buffers)
-  //   MMA issue: thread 0 of the leader, in chunk order, 3 MMAs per 8 columns of K
+  //   MMA issue: warp 0 of the leader (converged, one elected lane), in chunk order, 3 MMAs
+  //   per 8 columns of K
   //   (hi.hi + hi.lo + lo.hi); the accumulator takes TMEM columns [0, NB) once chunk 0 (those
   //   columns of h) has been read by every producer.
   constexpr int W2T = 2048;                        // bytes per chunk of B (hi or lo)
@@ -287,19 +293,22 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
   __syncthreads();
   {
     constexpr uint32_t idesc2 = idesc_tf32_f32(2 * WBM, NB);
-    auto issue = [&](int cc) {                     // leader, thread 0
+    auto issue = [&](int cc) {                     // leader CTA, warp 0 converged, one lane issues
       const int bf = cc % NA;
       mbar_wait(afull0 + 8 * bf, (uint32_t)(cc / NA) & 1u);
       tc_fence_after();
       const uint64_t ah = sw128_kmajor_desc(abuf + bf * 32768), al = sw128_kmajor_desc(abuf + bf * 32768 + 16384);
       const uint64_t bh = sw128_kmajor_desc(w2hi + cc * W2T), bl = sw128_kmajor_desc(w2lo + cc * W2T);
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {             // +32 bytes along K per 8 fp32
-        umma_tf32_pair(tmem, ah + 2 * kk, bh + 2 * kk, idesc2, (cc > 0 || kk > 0) ? 1u : 0u);
-        umma_tf32_pair(tmem, ah + 2 * kk, bl + 2 * kk, idesc2, 1u);
-        umma_tf32_pair(tmem, al + 2 * kk, bh + 2 * kk, idesc2, 1u);
+        for (int kk = 0; kk < 4; ++kk) {           // +32 bytes along K per 8 fp32
+          umma_tf32_pair(tmem, ah + 2 * kk, bh + 2 * kk, idesc2, (cc > 0 || kk > 0) ? 1u : 0u);
+          umma_tf32_pair(tmem, ah + 2 * kk, bl + 2 * kk, idesc2, 1u);
+          umma_tf32_pair(tmem, al + 2 * kk, bh + 2 * kk, idesc2, 1u);
+        }
+        umma_commit_pair(afree0 + 8 * bf);
       }
-      umma_commit_pair(afree0 + 8 * bf);
+      __syncwarp();
     };
     const int g = warp & 3, par = warp >> 2, row = 32 * g + lane;
     const int rb = (row >> 3) * 1024 + (row & 7) * 128;
@@ -326,17 +335,19 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(mapa(afull0 + 8 * bf, 0u));
-      if (r == 0 && warp == 0 && lane == 0)
-        for (int cc = c > 0 ? c - 1 : 0; cc <= c; ++cc) issue(cc);
       __syncwarp();
+      if (r == 0 && warp == 0)
+        for (int cc = c > 0 ? c - 1 : 0; cc <= c; ++cc) issue(cc);
     }
-    if (r == 0 && tid == 0) {
+    if (r == 0 && warp == 0) {
       issue(WH / 32 - 1);
-      umma_commit_pair(zdone);
+      if (elect_one()) umma_commit_pair(zdone);
+      __syncwarp();
     }
   }
   mbar_wait(zdone, 0);
   tc_fence_after();
+  if (tr && tid == 0) tr[3] = gtimer();
   float *zs2 = reinterpret_cast<float *>(smem + 32 * W2T);   // [WBM][KBP] over A buffer 0
   if (warp < 4) {
     uint32_t v[32];
@@ -345,24 +356,22 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
     for (int b = 0; b < KBP; ++b) zs2[(32 * warp + lane) * KBP + b] = __uint_as_float(v[b]);
   }
   __syncthreads();
-  // ---- head (row a3): one lane per bin, SEG-lane segments, rows spread over the 8 warps
-  {
-    const int SEG = k <= 16 ? 16 : 32;
-    const int per_warp = 32 / SEG, seg = lane / SEG, b = lane % SEG;
-    for (int base = warp * per_warp; base < WBM; base += (WT / 32) * per_warp) {
-      const int rr = base + seg;
-      const int j = m0 + rr < n ? m0 + rr : n;
-      float z = 0.f;
-      if (j < n && b < k)
-        z = __ldg(b2 + b) + zs2[rr * KBP + b];
-      head_seg(j, n, k, SEG, b, z, hs, cst.dyn_c, j < n ? s_slot[rr] : 0xFFFFFFFFu, s_meta[rr],
-               b < KB ? s_lq[rr * KB + (b < KB ? b : 0)] : -INFINITY, prior_override, lq_state,
-               meta, post, Lout, err);
+  // ---- head (row a3): one thread per row, all k bins in registers (head_row)
+  if (tid < WBM) {
+    const int rr = tid, j = m0 + rr;
+    if (j < n) {
+      float z[KB];
+#pragma unroll
+      for (int b = 0; b < KB; ++b) z[b] = b < k ? __ldg(b2 + b) + zs2[rr * KBP + b] : 0.f;
+      head_row<KB>(j, k, z, hs, cst.dyn_c, s_slot[rr], s_meta[rr], s_lq + rr * KB, prior_override,
+                   lq_state, meta, post, Lout, err);
     }
   }
+  if (tr && tid == 0) tr[4] = gtimer();
   tc_fence_before();
   cluster_sync();                    // both CTAs done with TMEM
   if (warp == 0) tmem_dealloc_pair(tmem, (uint32_t)WH);
+  if (tr && tid == 0) tr[5] = gtimer();
 }
 
 // ------------------------------------------------------------------ host
@@ -441,7 +450,8 @@ cudaError_t launch_wide_predict(Ctx &c, const void *emb, int64_t ld, const int32
                             n, c.d / WBK, (const float *)c.b1, (const float *)c.w2,              \
                             (const float *)c.b2, c.host_consts, ids, is_prefill, prior_override, \
                             c.cfg.max_slots, c.lq, c.meta, post, L, c.dev_err, decode_only,     \
-                            wide_flags())
+                            wide_flags(),                                                         \
+                            (c.trace && (int)cfg.gridDim.x <= c.trace_cap) ? c.trace : nullptr)
   switch (wide_kb(c.k)) {
     case 10: TRAIL_WIDE(10);
     case 16: TRAIL_WIDE(16);
