@@ -36,6 +36,14 @@ for rep in range(3):
     tr = tr[(tr[:, 0] > 0) & (tr[:, 5] > 0)]
     t0 = tr[:, 0].min()
     ph = lambda i, j: [int(np.median(tr[:, j] - tr[:, i])), int((tr[:, j] - tr[:, i]).max())]  # noqa: E731
+    # CTAs whose 128 rows hold a prompt (their X rows come from K1's xs: they wait for K1)
+    pf = np.asarray(b.is_prefill).astype(bool)
+    has_p = np.array([pf[128 * c:128 * c + 128].any() for c in range(len(tr))])
+    kl = tr[:, 2] - tr[:, 1]
+    extra = {"k_loop_prompt_ctas": [int(np.median(kl[has_p])) if has_p.any() else -1, int(has_p.sum())],
+             "k_loop_decode_ctas": [int(np.median(kl[~has_p])), int(kl[~has_p].max()), int((~has_p).sum())],
+             "start_prompt_ctas": int(np.median(tr[has_p, 0] - t0)) if has_p.any() else -1}
+    print(json.dumps(extra), flush=True)
     print(json.dumps({"diag": os.environ.get("TRAIL_WIDE_DIAG", "0"), "ctas": len(tr),
                       "start_skew": int(tr[:, 0].max() - t0), "prologue": ph(0, 1), "k_loop": ph(1, 2),
                       "layer2": ph(2, 3), "head": ph(3, 4), "teardown": ph(4, 5),
