@@ -314,22 +314,25 @@ trail_wide_predict_kernel(const __grid_constant__ CUtensorMap tmap_emb,
     const int rb = (row >> 3) * 1024 + (row & 7) * 128;
     for (int c = par; c < WH / 32; c += 2) {
       const int bf = c % NA;
-      if (c >= NA) mbar_wait(afree0 + 8 * bf, (uint32_t)(c / NA - 1) & 1u);
+      // TMEM -> registers and the split before waiting for the buffer (only the stores need it)
       uint32_t v[32];
       tmem_ld32(tmem + ((uint32_t)(32 * g) << 16) + (uint32_t)(32 * c), v);
+      float hh[32], hl[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const float h = fmaxf(__uint_as_float(v[q]) + b1s[32 * c + q], 0.f);
+        hh[q] = tf32_hi(h);
+        hl[q] = h - hh[q];
+      }
+      if (c >= NA) mbar_wait(afree0 + 8 * bf, (uint32_t)(c / NA - 1) & 1u);
       uint8_t *ahi = smem + 32 * W2T + bf * 32768, *alo = ahi + 16384;
 #pragma unroll
       for (int q4 = 0; q4 < 8; ++q4) {
-        float h[4], hh[4], hl[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          h[e] = fmaxf(__uint_as_float(v[4 * q4 + e]) + b1s[32 * c + 4 * q4 + e], 0.f);
-          hh[e] = tf32_hi(h[e]);
-          hl[e] = h[e] - hh[e];
-        }
         const int off = rb + ((q4 ^ (row & 7)) << 4);
-        *reinterpret_cast<float4 *>(ahi + off) = make_float4(hh[0], hh[1], hh[2], hh[3]);
-        *reinterpret_cast<float4 *>(alo + off) = make_float4(hl[0], hl[1], hl[2], hl[3]);
+        *reinterpret_cast<float4 *>(ahi + off) =
+            make_float4(hh[4 * q4], hh[4 * q4 + 1], hh[4 * q4 + 2], hh[4 * q4 + 3]);
+        *reinterpret_cast<float4 *>(alo + off) =
+            make_float4(hl[4 * q4], hl[4 * q4 + 1], hl[4 * q4 + 2], hl[4 * q4 + 3]);
       }
       fence_proxy_async_smem();
       tc_fence_before();
