@@ -1,6 +1,6 @@
 """K2d timing probe at configs[3] shape (16 384 requests, d = 8192, k = 20): median per-launch
 time of the layer-1 kernel (profile mode: CUDA events around the launch), L2 flushed before
-every step.  Knobs come from the environment (TRAIL_WIDE_PF, TRAIL_WIDE_DIAG).  Diagnostic."""
+every step.  Knob: TRAIL_WIDE_DIAG (load-skipping probes).  Diagnostic."""
 import json
 import os
 import sys
@@ -28,7 +28,7 @@ torch.cuda.synchronize()
 fl = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 fl2 = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 trail_profile_enable(t.h, 1)
-out = {"pf": os.environ.get("TRAIL_WIDE_PF", "0"), "diag": os.environ.get("TRAIL_WIDE_DIAG", "0")}
+out = {"diag": os.environ.get("TRAIL_WIDE_DIAG", "0")}
 for name in ("umma", "pool"):
     trail_profile_read(t.h, name, reset=True)
 vals = {"umma": [], "pool": []}
